@@ -1,0 +1,28 @@
+# Builds the B200 library (sm_100a) and the CPU oracle (test infrastructure).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+SRC := $(wildcard paper_2411_06360_b200/csrc/*.cu)
+HDR := $(wildcard paper_2411_06360_b200/csrc/*.cuh) include/rsr_b200.h
+LIB := paper_2411_06360_b200/lib/librsr_b200.so
+OBJDIR := build/obj
+OBJ := $(patsubst paper_2411_06360_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
+
+all: $(LIB) oracle
+
+$(OBJDIR)/%.o: paper_2411_06360_b200/csrc/%.cu $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(LIB): $(OBJ)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RSR++ ternary matvec (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config ternary16384|binary16384|llama4096|llama4096x14336|llama14336x4096|ternary65536]
+
+One JSON line on stdout (rank 0).  A "step" is one RSR++ matvec v . A over the
+whole synthetic matrix with the index and v already resident in HBM (`value`);
+`e2e` is the same matvec through the reference-facing API with host buffers
+(`rsr.multiply_ternary(numpy_v, idx)`: H2D + kernel + D2H every step).
+
+L2 rule: each timed step multiplies against a different copy of the index
+(rotating >= 4 x L2 worth of index bytes), so no step reads an index the
+previous step left in L2.
+
+N > 1 (torchrun): weak scaling of the column-sharded matvec — rank g owns a
+full 16384 x 16384 shard (the columns [g*m, (g+1)*m) of a 16384 x (N*m)
+matrix), multiplies it, and the output slices are NCCL all-gathered every step
+(the north star's column-block sharding + all-gather).  value = N shard-matvecs
+per step / max-over-ranks time.
+
+--impl reference: the reference algorithm's CPU path (oracle/rsr_oracle.c, a C
+port of `_run_blocks` + `multiply_parallel`; the reference itself is Python +
+Numba and cannot travel to the GPU box) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (domain, n rows, m cols, workload description)
+    "ternary16384": ("ternary", 16384, 16384, "ternary 16384x16384 RSR++ matvec, k=11, int32 activations"),
+    "binary16384": ("binary", 16384, 16384, "binary 16384x16384 RSR++ matvec, k=11, int32 activations"),
+    "llama4096": ("ternary", 4096, 4096, "ternary 4096x4096 (Llama-3-8B q/o) RSR++ matvec, k=9"),
+    "llama4096x14336": ("ternary", 4096, 14336, "ternary 4096x14336 (Llama-3-8B gate/up) RSR++ matvec, k=9"),
+    "llama14336x4096": ("ternary", 14336, 4096, "ternary 14336x4096 (Llama-3-8B down) RSR++ matvec, k=11"),
+    "ternary65536": ("ternary", 65536, 65536, "ternary 65536x65536 RSR++ matvec, k=13"),
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _profile_traffic(config: str):
+    """DRAM bytes per launch of the top kernel from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s.get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_matrix(domain: str, n: int, m: int, seed: int = 0) -> np.ndarray:
+    """Reference convention (bench.py:80-84): default_rng([seed, n, m]) uniform entries."""
+    rng = np.random.default_rng([seed, n, m])
+    if domain == "ternary":
+        return rng.integers(-1, 2, size=(n, m), dtype=np.int8)
+    return rng.integers(0, 2, size=(n, m), dtype=np.int8)
+
+
+def make_vector(n: int, seed: int = 0) -> np.ndarray:
+    """Integer activations in [-100, 100] (bench.py:85)."""
+    return np.random.default_rng([seed, n, 1]).integers(-100, 101, size=n).astype(np.int32)
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_cpu_reference(A: np.ndarray, v: np.ndarray, k: int, domain: str, min_seconds: float = 5.0,
+                       workers: int | None = None):
+    """The reference algorithm on host cores (C port), mean seconds per full matvec.
+    Warm-up 3 (bench.py:18,35-43), then repeat until min_seconds of samples."""
+    from oracle import c_oracle
+    workers = workers or cpu_threads()
+    n, m = A.shape
+    kp = c_oracle.keys_ternary(A, k, 1)
+    kn = c_oracle.keys_ternary(A, k, -1) if domain == "ternary" else None
+    v64 = v.astype(np.float64)
+    run = lambda: c_oracle.multiply_parallel(v64, kp, kn, m, k, True, workers)  # noqa: E731
+    for _ in range(3):
+        out = run()
+    samples = []
+    t_end = time.perf_counter() + min_seconds
+    while time.perf_counter() < t_end or len(samples) < 3:
+        t0 = time.perf_counter()
+        run()
+        samples.append(time.perf_counter() - t0)
+    return float(np.mean(samples)), len(samples), workers, out
+
+
+def run_reference(args, cfg):
+    """--impl reference: rank 0 only, the C port of the reference CPU path."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    domain, n, m, desc = cfg
+    from paper_2411_06360_b200.indexer import optimal_k_rsrpp
+    k = optimal_k_rsrpp(n)
+    A = make_matrix(domain, n, m)
+    v = make_vector(n)
+    from oracle import c_oracle
+    workers = cpu_threads()
+    kp = c_oracle.keys_ternary(A, k, 1)
+    kn = c_oracle.keys_ternary(A, k, -1) if domain == "ternary" else None
+    v64 = v.astype(np.float64)
+    for _ in range(max(args.warmup, 0)):
+        c_oracle.multiply_parallel(v64, kp, kn, m, k, True, workers)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        c_oracle.multiply_parallel(v64, kp, kn, m, k, True, workers)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = 1.0 / dt
+    line = {
+        "impl": "reference", "metric": "ternary RSR++ matvec vectors/sec", "value": value,
+        "unit": "vectors/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "n": n, "m": m, "k": k, "batch": 1},
+        "cpu_baseline": {"value": value, "unit": "vectors/s", "cores": workers, "kind": "port",
+                         "sample": f"{args.steps} full {n}x{m} RSR++ matvecs (C port of kernels.py:127-239)"},
+        "e2e": {"value": value, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import paper_2411_06360_b200 as rsr
+    from paper_2411_06360_b200 import _native
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    domain, n, m, desc = cfg
+    k = rsr.optimal_k_rsrpp(n)
+
+    # ---- data: rank g's shard = columns [g*m, (g+1)*m) of the n x (N*m) matrix
+    A = make_matrix(domain, n, m, seed=rank)
+    v = make_vector(n)
+    t0 = time.perf_counter()
+    dA = torch.from_numpy(A).cuda()
+    if domain == "ternary":
+        idx = rsr.preprocess_ternary(dA, k)
+    else:
+        idx = rsr.preprocess(rsr.BinaryMatrix.from_dense(A.astype(np.uint8)), k)
+    torch.cuda.synchronize()
+    preprocess_s = time.perf_counter() - t0
+
+    # ---- parity gate at full size (untimed): GPU keys + product vs the C oracle
+    from oracle import c_oracle
+    kp = c_oracle.keys_ternary(A, k, 1)
+    kn = c_oracle.keys_ternary(A, k, -1) if domain == "ternary" else None
+    halves = [idx.positive, idx.negative] if domain == "ternary" else [idx]
+    for h, keys in zip(halves, [kp, kn]):
+        if not np.array_equal(h.device_tensors()["bucket"][:, :n].cpu().numpy(), keys):
+            raise SystemExit("parity failure: device keys differ from the oracle")
+    ref = c_oracle.multiply_parallel(v.astype(np.float64), kp, kn, m, k, True, cpu_threads())
+    dv = torch.from_numpy(v).cuda()
+    got = rsr.multiply_ternary(dv, idx) if domain == "ternary" else rsr.multiply_rsr(dv, idx)
+    if not np.array_equal(got.cpu().numpy().astype(np.float64), ref):
+        raise SystemExit("parity failure: device product differs from the oracle")
+    del A, dA
+
+    # ---- index copies so consecutive steps never hit an index left in L2
+    def clone_index(src):
+        import copy
+        from paper_2411_06360_b200.indexer import RsrIndex, TernaryIndex
+        arrays = copy.copy(src.positive._arrays if domain == "ternary" else src._arrays)
+        a0 = src.positive._arrays if domain == "ternary" else src._arrays
+        arrays.perm = [t.clone() for t in a0.perm]
+        arrays.seg = [t.clone() for t in a0.seg]
+        arrays.bucket = [t.clone() for t in a0.bucket]
+        arrays.desc = _native.IndexDesc.from_buffer_copy(a0.desc)
+        for h in range(len(arrays.perm)):
+            arrays.desc.half[h].perm = arrays.perm[h].data_ptr()
+            arrays.desc.half[h].seg = arrays.seg[h].data_ptr()
+            arrays.desc.half[h].bucket = arrays.bucket[h].data_ptr()
+        if domain == "ternary":
+            return TernaryIndex(RsrIndex(arrays, 0), RsrIndex(arrays, 1))
+        return RsrIndex(arrays, 0)
+
+    nblocks = idx.desc.nblocks
+    hv = len(halves)
+    row_stride = idx.desc.row_stride
+    read_bytes = hv * nblocks * row_stride * 2 + 4 * n + 4 * m          # bucket u16 + v + out (scatter)
+    seg_stride = idx.desc.seg_stride
+    canonical = hv * sum(2 * n + 4 * (1 << min(k, m - b * k)) for b in range(nblocks)) + 4 * n + 4 * m
+    ncopies = max(2, -(-4 * L2_BYTES // (hv * nblocks * row_stride * 2)))
+    copies = [idx] + [clone_index(idx) for _ in range(ncopies - 1)]
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    out = torch.empty(m, dtype=torch.int32, device="cuda")
+    mult = rsr.multiply_ternary if domain == "ternary" else rsr.multiply_rsr
+    gathered = torch.empty(world * m, dtype=torch.int32, device="cuda") if world > 1 else None
+
+    from paper_2411_06360_b200 import kernels as K
+
+    def step(i):
+        K._multiply_device(dv, copies[i % ncopies], True, None, out)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out)
+
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+
+    # The timed K steps are one CUDA-graph replay: a 20 us kernel launched from Python
+    # would be launch-bound, a graph issues the K launches back to back.
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(stream)
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(graph, stream=cap):
+            for i in range(args.steps):
+                K._multiply_device(dv, copies[i % ncopies], True, None, out)
+                if world > 1:
+                    dist.all_gather_into_tensor(gathered, out)
+    stream.wait_stream(cap)
+    graph.replay()  # warm the graph itself
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        t_load = time.perf_counter() + 0.6
+        while time.perf_counter() < t_load:       # load before the timed region (clocks settle)
+            graph.replay()
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_begin.record(stream)
+        graph.replay()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        t_load = time.perf_counter() + 0.3
+        while time.perf_counter() < t_load:       # and after it, so the sampler brackets it
+            graph.replay()
+            torch.cuda.synchronize()
+    total_ms = t_begin.elapsed_time(t_end)
+    kernel_ms = [total_ms / args.steps]
+    if world > 1:
+        tt = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    value = world * 1e3 / ms_per_step  # shard-matvecs (16384^2-equivalents) per second
+
+    # ---- e2e through the reference-facing API with host buffers (rank-local)
+    v_host = v.copy()
+    for i in range(3):
+        mult(v_host, copies[i % ncopies])
+    torch.cuda.synchronize()
+    e2e_steps = min(max(args.steps, 20), 500)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(e2e_steps):
+        res = mult(v_host, copies[i % ncopies])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if not np.array_equal(res, ref):
+        raise SystemExit("parity failure on the e2e path")
+
+    peak, peak_kind = _peaks()
+    avg_kernel_s = statistics.mean(kernel_ms) / 1e3
+    achieved = read_bytes / avg_kernel_s / 1e9
+    line = {
+        "metric": "ternary RSR++ matvec vectors/sec" if domain == "ternary" else "binary RSR++ matvec vectors/sec",
+        "value": value, "unit": "vectors/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int32", "data": "synthetic",
+        "config": {"workload": desc + (f"; {world} column shards + NCCL all-gather" if world > 1 else ""),
+                   "n": n, "m": m, "k": k, "batch": 1, "l2": f"rotating {ncopies} index copies (>= 4x L2)",
+                   "form": "scatter", "preprocess_s": round(preprocess_s, 4)},
+        "gpu_launches": args.steps * (1 if idx.desc.rows <= 16384 else 2),
+        "e2e": {"value": 1e3 / e2e_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * n,
+                "d2h_bytes_per_step": 8 * m, "path": "rsr.multiply_ternary(numpy int32 v, idx)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _profile_traffic(args.config),
+                     "peak_kind": peak_kind, "algorithmic_bytes": read_bytes,
+                     "canonical_gather_bytes": canonical,
+                     "canonical_gbs": canonical / avg_kernel_s / 1e9,
+                     "kernel_us": avg_kernel_s * 1e6},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_s, reps, workers, _ = time_cpu_reference(make_matrix(domain, n, m), v, k, domain,
+                                                     min_seconds=args.cpu_seconds)
+        line["cpu_baseline"] = {"value": 1.0 / cpu_s, "unit": "vectors/s", "cores": workers, "kind": "port",
+                                "sample": f"{reps} full {n}x{m} RSR++ matvecs, fp64, C port of "
+                                          "kernels.py:127-239 on {workers} threads".replace("{workers}", str(workers))}
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="ternary16384", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

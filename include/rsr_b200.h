@@ -1,0 +1,142 @@
+/*
+ * rsr_b200.h — C ABI of the B200-native RSR / RSR++ library (librsr_b200.so).
+ *
+ * The reference (arxiv 2411.06360, /root/reference/pkg/src/rsr) is a Python +
+ * Numba package with no C ABI; its compiled entry points are Numba functions
+ * called from Python.  Each function below replaces one of them (cited
+ * file:line), with plain pointers and sizes and no torch types, so any host
+ * (Python ctypes, C, C++) can bind it.  INTEGRATION.md shows the ctypes stub
+ * the reference's `rsr.kernels` would use.
+ *
+ * Conventions
+ *  - Device pointers unless a name ends in `_host`.  Kernels are enqueued on
+ *    `stream` (a cudaStream_t, NULL = legacy default stream); nothing
+ *    synchronizes except the `_host` entry points.
+ *  - Every call returns an rsr_status; rsr_b200_last_error() returns a
+ *    thread-local message for the last failure.  RSR_ERR_INVALID messages use
+ *    the reference's wording ("does not match", "variant", "k must be in ...")
+ *    so the Python layer can raise the same ValueError.
+ *  - No CPU fallback exists: if there is no usable sm_100 device the call
+ *    fails with RSR_ERR_CUDA.
+ */
+#ifndef RSR_B200_H_
+#define RSR_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSR_B200_ABI_VERSION 1
+
+typedef enum rsr_status {
+  RSR_OK = 0,
+  RSR_ERR_INVALID = 1,     /* bad argument (maps to ValueError) */
+  RSR_ERR_UNSUPPORTED = 2, /* valid for the reference but beyond a device limit (e.g. k > 15) */
+  RSR_ERR_CUDA = 3,        /* CUDA runtime failure */
+} rsr_status;
+
+typedef enum rsr_dtype { RSR_I32 = 0, RSR_F32 = 1, RSR_F64 = 2 } rsr_dtype;
+
+/* kernels.py:14-21 `_VARIANTS`: "rsr" -> dense block product, "rsrpp"/"rsr++" -> fold. */
+typedef enum rsr_variant { RSR_VARIANT_RSR = 0, RSR_VARIANT_RSRPP = 1 } rsr_variant;
+
+/* Multiply formulation.  AUTO picks SCATTER for int32 activations and GATHER
+ * otherwise (no native fp32 shared-memory atomic add exists on sm_100). */
+typedef enum rsr_form { RSR_FORM_AUTO = 0, RSR_FORM_SCATTER = 1, RSR_FORM_GATHER = 2 } rsr_form;
+
+/* One binary matrix's index: the device image of the reference RsrIndex
+ * (indexer.py:47-139).  Arrays are block-major; block b covers columns
+ * [b*k, b*k + w_b), w_b = min(k, cols - b*k) (column_blocks, indexer.py:193-199). */
+typedef struct rsr_half_index {
+  void* perm;       /* [nblocks][row_stride] u16 if rows <= 65536 else u32:
+                       stable row order per block (indexer.py:269); entries >= rows are 0 */
+  uint32_t* seg;    /* [nblocks][seg_stride]: seg[j] = #rows with key < j for
+                       j < 2^w, seg[2^w] = rows (indexer.py:274-276 incl. sentinel) */
+  uint16_t* bucket; /* [nblocks][row_stride]: key of every row, MSB-first
+                       (indexer.py:270 `_buckets`); padding rows hold 0 */
+} rsr_half_index;
+
+typedef struct rsr_index_desc {
+  int64_t rows, cols;
+  int32_t k;          /* block width, 1 <= k <= 16 on the device */
+  int32_t nblocks;    /* ceil(cols / k) */
+  int32_t perm_bytes; /* 2 or 4 */
+  int32_t halves;     /* 1 = binary index; 2 = ternary (half[0] positive, half[1] negative) */
+  int64_t row_stride; /* rows rounded up to a multiple of 8 (16-byte rows for TMA) */
+  int64_t seg_stride; /* 2^k + 1 */
+  rsr_half_index half[2];
+} rsr_index_desc;
+
+int rsr_b200_abi_version(void);
+const char* rsr_b200_last_error(void);
+
+/* Fill the size fields of `desc` (pointers untouched) and report the bytes of each
+ * array per half.  Validates k as `_check_k` does (indexer.py:19-23). */
+rsr_status rsr_index_layout(int64_t rows, int64_t cols, int32_t k, int32_t halves,
+                            rsr_index_desc* desc, size_t* perm_bytes, size_t* seg_bytes,
+                            size_t* bucket_bytes);
+
+/* Device workspace bytes rsr_preprocess_* needs for this index. */
+size_t rsr_preprocess_workspace_bytes(const rsr_index_desc* desc);
+
+/* Replaces preprocess_ternary (indexer.py:281-286) = decompose_ternary
+ * (core.py:124-128) + preprocess (indexer.py:251-278) for both halves.
+ * A: int8 [rows][lda] row-major, entries must be -1/0/+1.  Any other entry sets
+ * *d_bad_entries (device int32, caller-zeroed) to a nonzero count — the
+ * TernaryMatrix alphabet check (core.py:33). */
+rsr_status rsr_preprocess_ternary(const int8_t* A, int64_t lda, const rsr_index_desc* desc,
+                                  int32_t* d_bad_entries, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
+/* Replaces preprocess (indexer.py:251-278) for a BinaryMatrix stored as the
+ * reference stores it (core.py:53-99): bits [rows][ldb] bytes, MSB-first. */
+rsr_status rsr_preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_desc* desc,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Replaces `_run_blocks` over blocks [block_begin, block_end) of every half
+ * (kernels.py:127-177) followed by the `pos - neg` of multiply_ternary
+ * (kernels.py:196-206) or the single half of multiply_rsr (kernels.py:185-193).
+ * v: [rows] of v_dtype.  out: [cols] of out_dtype; only columns of the block
+ * range are written (multiply_parallel's disjoint slices, kernels.py:209-239).
+ * int32 accumulation is exact modulo 2^32 (bit-exact whenever the true result
+ * fits); out_dtype may be F64 for int32 input (reference result type). */
+rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_dtype, void* out,
+                        rsr_dtype out_dtype, rsr_variant variant, rsr_form form,
+                        int32_t block_begin, int32_t block_end, void* stream);
+
+/* Batched multiply: V [batch][rows] -> OUT [batch][cols] (same dtype rules). */
+rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_dtype v_dtype,
+                                int64_t batch, void* OUT, rsr_dtype out_dtype,
+                                rsr_variant variant, void* stream);
+
+/* End-to-end entry with HOST buffers (the call a reference-side binding makes):
+ * copies v_host -> d_v, multiplies all blocks, copies d_out -> out_host and
+ * synchronizes the stream.  d_v / d_out are caller-owned device scratch of the
+ * right size; v_host / out_host should be pinned for async copies. */
+rsr_status rsr_multiply_host(const rsr_index_desc* desc, const void* v_host, rsr_dtype v_dtype,
+                             void* out_host, rsr_dtype out_dtype, rsr_variant variant,
+                             void* d_v, void* d_out, void* stream);
+
+/* Replaces segmented_sum / `_segment_sums` (kernels.py:50-60, 94-101): gather-form
+ * bucket sums u[0..2^w) of one block of one half. */
+rsr_status rsr_segmented_sum(const rsr_index_desc* desc, int32_t half, int32_t block,
+                             const void* v, rsr_dtype dtype, void* u, void* stream);
+
+/* Replaces block_product_rsr / block_product_rsrpp (kernels.py:104-116, loops at
+ * kernels.py:63-91) for one SegmentedSums vector u[0..2^width) (fp64); buf holds
+ * 2^(width-1) doubles of scratch, out receives `width` doubles. */
+rsr_status rsr_block_product(const double* u, int32_t width, rsr_variant variant, double* buf, double* out,
+                             void* stream);
+
+/* Replaces naive_multiply (core.py:135-169) for a ternary int8 matrix: the
+ * "standard" dense multiply, on the GPU (the honest dense comparator). */
+rsr_status rsr_naive_multiply_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t lda,
+                                      const void* v, rsr_dtype dtype, void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSR_B200_H_ */

@@ -1,0 +1,116 @@
+"""ctypes binding of the C ABI in include/rsr_b200.h (librsr_b200.so).
+
+The library is the product: every multiply / preprocess call goes through it.
+There is no CPU fallback — if the library (or a CUDA device) is missing, the
+call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "librsr_b200.so")
+
+RSR_OK, RSR_ERR_INVALID, RSR_ERR_UNSUPPORTED, RSR_ERR_CUDA = 0, 1, 2, 3
+I32, F32, F64 = 0, 1, 2
+VARIANT_RSR, VARIANT_RSRPP = 0, 1
+FORM_AUTO, FORM_SCATTER, FORM_GATHER = 0, 1, 2
+
+ABI_VERSION = 1
+
+# Every symbol include/rsr_b200.h declares (tests check the .so exports them all).
+EXPORTS = (
+    "rsr_b200_abi_version", "rsr_b200_last_error", "rsr_index_layout",
+    "rsr_preprocess_workspace_bytes", "rsr_preprocess_ternary", "rsr_preprocess_binary",
+    "rsr_multiply", "rsr_multiply_batched", "rsr_multiply_host", "rsr_segmented_sum",
+    "rsr_block_product", "rsr_naive_multiply_ternary",
+)
+
+
+class HalfIndex(ctypes.Structure):
+    _fields_ = [("perm", ctypes.c_void_p), ("seg", ctypes.c_void_p), ("bucket", ctypes.c_void_p)]
+
+
+class IndexDesc(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+        ("k", ctypes.c_int32), ("nblocks", ctypes.c_int32),
+        ("perm_bytes", ctypes.c_int32), ("halves", ctypes.c_int32),
+        ("row_stride", ctypes.c_int64), ("seg_stride", ctypes.c_int64),
+        ("half", HalfIndex * 2),
+    ]
+
+
+class NativeError(RuntimeError):
+    """A CUDA-side failure inside librsr_b200.so."""
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"librsr_b200.so not found at {LIB_PATH}; build it with `make` "
+            "(or __graft_entry__.build()). There is no CPU fallback.")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I64, I32_, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+    st = ctypes.c_int
+    L.rsr_b200_abi_version.restype = ctypes.c_int
+    L.rsr_b200_last_error.restype = ctypes.c_char_p
+    L.rsr_index_layout.argtypes = [I64, I64, I32_, I32_, ctypes.POINTER(IndexDesc),
+                                   ctypes.POINTER(SZ), ctypes.POINTER(SZ), ctypes.POINTER(SZ)]
+    L.rsr_index_layout.restype = st
+    L.rsr_preprocess_workspace_bytes.argtypes = [ctypes.POINTER(IndexDesc)]
+    L.rsr_preprocess_workspace_bytes.restype = SZ
+    L.rsr_preprocess_ternary.argtypes = [P, I64, ctypes.POINTER(IndexDesc), P, P, SZ, P]
+    L.rsr_preprocess_ternary.restype = st
+    L.rsr_preprocess_binary.argtypes = [P, I64, ctypes.POINTER(IndexDesc), P, SZ, P]
+    L.rsr_preprocess_binary.restype = st
+    L.rsr_multiply.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_int, I32_, I32_, P]
+    L.rsr_multiply.restype = st
+    L.rsr_multiply_batched.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, I64, P,
+                                       ctypes.c_int, ctypes.c_int, P]
+    L.rsr_multiply_batched.restype = st
+    L.rsr_multiply_host.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
+                                    ctypes.c_int, P, P, P]
+    L.rsr_multiply_host.restype = st
+    L.rsr_segmented_sum.argtypes = [ctypes.POINTER(IndexDesc), I32_, I32_, P, ctypes.c_int, P, P]
+    L.rsr_segmented_sum.restype = st
+    L.rsr_block_product.argtypes = [P, I32_, ctypes.c_int, P, P, P]
+    L.rsr_block_product.restype = st
+    L.rsr_naive_multiply_ternary.argtypes = [P, I64, I64, I64, P, ctypes.c_int, P, P]
+    L.rsr_naive_multiply_ternary.restype = st
+    if L.rsr_b200_abi_version() != ABI_VERSION:
+        raise ImportError("librsr_b200.so ABI version mismatch; rebuild with `make`")
+    _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    """Map an rsr_status to the reference's exception types."""
+    if status == RSR_OK:
+        return
+    msg = (lib().rsr_b200_last_error() or b"").decode()
+    if status in (RSR_ERR_INVALID, RSR_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    raise NativeError(msg)
+
+
+def layout(rows: int, cols: int, k: int, halves: int):
+    desc = IndexDesc()
+    pb, sb, bb = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    check(lib().rsr_index_layout(rows, cols, k, halves, ctypes.byref(desc),
+                                 ctypes.byref(pb), ctypes.byref(sb), ctypes.byref(bb)))
+    return desc, pb.value, sb.value, bb.value
+
+
+def current_stream_ptr() -> int:
+    import torch
+    return torch.cuda.current_stream().cuda_stream

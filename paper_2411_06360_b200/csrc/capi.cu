@@ -1,0 +1,203 @@
+// extern "C" entry points of librsr_b200.so (declared in include/rsr_b200.h).
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace rsr {
+
+// implemented in preprocess.cu / multiply.cu
+size_t preprocess_workspace_bytes(const rsr_index_desc* d);
+rsr_status preprocess_ternary(const int8_t* A, int64_t lda, const rsr_index_desc* d, int32_t* bad, void* ws,
+                              size_t ws_bytes, cudaStream_t s);
+rsr_status preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_desc* d, void* ws, size_t ws_bytes,
+                             cudaStream_t s);
+rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
+                    rsr_form form, int b0, int b1, cudaStream_t s);
+rsr_status segmented_sum(const rsr_index_desc& d, int half, int block, const void* v, rsr_dtype dt, void* u,
+                         cudaStream_t s);
+rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t lda, const void* v, rsr_dtype dt,
+                         void* out, cudaStream_t s);
+rsr_status block_product(const double* u, int w, int use_fold, double* buf, double* out, cudaStream_t s);
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+rsr_status fail(rsr_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+rsr_status cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RSR_OK;
+  return fail(RSR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Per-device attribute cache (queried once; safe to call while a stream is capturing).
+namespace {
+constexpr int kMaxDevices = 64;
+int g_sm_count[kMaxDevices];
+int g_smem_optin[kMaxDevices];
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+}  // namespace
+
+int device_sm_count() {
+  const int dev = current_device();
+  if (!g_sm_count[dev]) {
+    int n = kSmSlots;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sm_count[dev] = n;
+  }
+  return g_sm_count[dev];
+}
+
+size_t device_max_smem_optin() {
+  const int dev = current_device();
+  if (!g_smem_optin[dev]) {
+    int n = 227 * 1024;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    g_smem_optin[dev] = n;
+  }
+  return (size_t)g_smem_optin[dev];
+}
+
+static rsr_status check_k(int64_t rows, int32_t k) {
+  // indexer.py:19-23 `_check_k` (same messages)
+  if (k < 1 || k > 30) return fail(RSR_ERR_INVALID, "k must be in [1, 30], got " + std::to_string(k));
+  int64_t maxk = 1;
+  for (int64_t r = rows; r > 1; r >>= 1) ++maxk;
+  maxk = std::max<int64_t>(1, std::min<int64_t>(30, maxk - 1));
+  if (k > maxk)
+    return fail(RSR_ERR_INVALID,
+                "k=" + std::to_string(k) + " exceeds max " + std::to_string(maxk) + " for " + std::to_string(rows) + " rows");
+  if (k > kMaxDeviceK) return fail(RSR_ERR_UNSUPPORTED, "k=" + std::to_string(k) + " exceeds the device limit of 16");
+  return RSR_OK;
+}
+
+static rsr_status check_range(const rsr_index_desc* d, int32_t b0, int32_t b1) {
+  if (!d) return fail(RSR_ERR_INVALID, "null index descriptor");
+  if (b0 < 0 || b1 > d->nblocks || b0 > b1) return fail(RSR_ERR_INVALID, "block range out of bounds");
+  if (d->halves != 1 && d->halves != 2) return fail(RSR_ERR_INVALID, "halves must be 1 or 2");
+  return RSR_OK;
+}
+
+}  // namespace rsr
+
+using namespace rsr;
+
+extern "C" {
+
+int rsr_b200_abi_version(void) { return RSR_B200_ABI_VERSION; }
+
+const char* rsr_b200_last_error(void) { return g_last_error.c_str(); }
+
+rsr_status rsr_index_layout(int64_t rows, int64_t cols, int32_t k, int32_t halves, rsr_index_desc* desc,
+                            size_t* perm_bytes, size_t* seg_bytes, size_t* bucket_bytes) {
+  if (rows < 1 || cols < 1) return fail(RSR_ERR_INVALID, "index dimensions must be at least 1x1");
+  if (halves != 1 && halves != 2) return fail(RSR_ERR_INVALID, "halves must be 1 or 2");
+  rsr_status st = check_k(rows, k);
+  if (st != RSR_OK) return st;
+  if (!desc) return fail(RSR_ERR_INVALID, "null index descriptor");
+  std::memset(desc, 0, sizeof(*desc));
+  desc->rows = rows;
+  desc->cols = cols;
+  desc->k = k;
+  desc->nblocks = (int32_t)((cols + k - 1) / k);
+  desc->perm_bytes = rows <= 65536 ? 2 : 4;
+  desc->halves = halves;
+  desc->row_stride = (rows + 7) / 8 * 8;
+  desc->seg_stride = ((int64_t)1 << k) + 1;
+  const size_t nb = (size_t)desc->nblocks;
+  if (perm_bytes) *perm_bytes = nb * desc->row_stride * desc->perm_bytes;
+  if (seg_bytes) *seg_bytes = nb * desc->seg_stride * sizeof(uint32_t);
+  if (bucket_bytes) *bucket_bytes = nb * desc->row_stride * sizeof(uint16_t);
+  return RSR_OK;
+}
+
+size_t rsr_preprocess_workspace_bytes(const rsr_index_desc* desc) {
+  return desc ? preprocess_workspace_bytes(desc) : 0;
+}
+
+rsr_status rsr_preprocess_ternary(const int8_t* A, int64_t lda, const rsr_index_desc* desc, int32_t* d_bad_entries,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  return preprocess_ternary(A, lda, desc, d_bad_entries, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+rsr_status rsr_preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_desc* desc, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  return preprocess_binary(bits, ldb, desc, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_dtype, void* out, rsr_dtype out_dtype,
+                        rsr_variant variant, rsr_form form, int32_t block_begin, int32_t block_end, void* stream) {
+  rsr_status st = check_range(desc, block_begin, block_end);
+  if (st != RSR_OK) return st;
+  if (!v || !out) return fail(RSR_ERR_INVALID, "null vector or output");
+  if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
+    return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
+  return multiply(*desc, v, v_dtype, out, out_dtype, variant, form, block_begin, block_end, (cudaStream_t)stream);
+}
+
+rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_dtype v_dtype, int64_t batch, void* OUT,
+                                rsr_dtype out_dtype, rsr_variant variant, void* stream) {
+  rsr_status st = check_range(desc, 0, desc ? desc->nblocks : 0);
+  if (st != RSR_OK) return st;
+  if (batch < 0) return fail(RSR_ERR_INVALID, "batch must be non-negative");
+  const size_t vsz = v_dtype == RSR_F64 ? 8 : 4, osz = out_dtype == RSR_F64 ? 8 : 4;
+  for (int64_t i = 0; i < batch; ++i) {
+    st = multiply(*desc, (const char*)V + i * desc->rows * vsz, v_dtype, (char*)OUT + i * desc->cols * osz, out_dtype,
+                  variant, RSR_FORM_AUTO, 0, desc->nblocks, (cudaStream_t)stream);
+    if (st != RSR_OK) return st;
+  }
+  return RSR_OK;
+}
+
+rsr_status rsr_multiply_host(const rsr_index_desc* desc, const void* v_host, rsr_dtype v_dtype, void* out_host,
+                             rsr_dtype out_dtype, rsr_variant variant, void* d_v, void* d_out, void* stream) {
+  rsr_status st = check_range(desc, 0, desc ? desc->nblocks : 0);
+  if (st != RSR_OK) return st;
+  if (!v_host || !out_host || !d_v || !d_out) return fail(RSR_ERR_INVALID, "null buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t vsz = v_dtype == RSR_F64 ? 8 : 4, osz = out_dtype == RSR_F64 ? 8 : 4;
+  if ((st = cuda_check(cudaMemcpyAsync(d_v, v_host, desc->rows * vsz, cudaMemcpyHostToDevice, s), "H2D v")) != RSR_OK)
+    return st;
+  if ((st = multiply(*desc, d_v, v_dtype, d_out, out_dtype, variant, RSR_FORM_AUTO, 0, desc->nblocks, s)) != RSR_OK)
+    return st;
+  if ((st = cuda_check(cudaMemcpyAsync(out_host, d_out, desc->cols * osz, cudaMemcpyDeviceToHost, s), "D2H out")) !=
+      RSR_OK)
+    return st;
+  return cuda_check(cudaStreamSynchronize(s), "stream sync");
+}
+
+rsr_status rsr_segmented_sum(const rsr_index_desc* desc, int32_t half, int32_t block, const void* v, rsr_dtype dtype,
+                             void* u, void* stream) {
+  rsr_status st = check_range(desc, 0, desc ? desc->nblocks : 0);
+  if (st != RSR_OK) return st;
+  if (half < 0 || half >= desc->halves || block < 0 || block >= desc->nblocks)
+    return fail(RSR_ERR_INVALID, "half or block out of range");
+  return segmented_sum(*desc, half, block, v, dtype, u, (cudaStream_t)stream);
+}
+
+rsr_status rsr_naive_multiply_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t lda, const void* v,
+                                      rsr_dtype dtype, void* out, void* stream) {
+  if (!A || !v || !out || rows < 1 || cols < 1 || lda < cols) return fail(RSR_ERR_INVALID, "bad naive arguments");
+  return naive_ternary(A, rows, cols, lda, v, dtype, out, (cudaStream_t)stream);
+}
+
+rsr_status rsr_block_product(const double* u, int32_t width, rsr_variant variant, double* buf, double* out,
+                             void* stream) {
+  if (!u || !buf || !out) return fail(RSR_ERR_INVALID, "null buffer");
+  if (width < 1 || width > 30) return fail(RSR_ERR_INVALID, "sums length must be 2^" + std::to_string(width));
+  if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
+    return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
+  return block_product(u, width, variant == RSR_VARIANT_RSRPP, buf, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

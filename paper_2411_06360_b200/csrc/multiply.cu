@@ -1,0 +1,636 @@
+// sm_100a multiply kernels for RSR / RSR++ (arxiv 2411.06360).
+//
+// Two formulations of the reference hot loop, both computing, per column block
+// b of width w, the bucket sums u_b[j] and the block product r_b = u_b . Bin_w:
+//
+//  * SCATTER (int32 activations) — the reference's own fused driver
+//    `_run_blocks` (kernels.py:127-177): u_b[key_b[r]] += v[r] over rows r.
+//    One persistent CTA per SM keeps its slice of v in REGISTERS for the whole
+//    launch, streams the per-block key rows (u16, `_buckets`) into a shared-
+//    memory ring with 1-D TMA bulk copies (mbarrier completion, L2 evict_first),
+//    and accumulates a 2^k-bin histogram with shared-memory int32 atomics
+//    (native ATOMS.ADD on sm_100; measured as fast as a random LDS).  Ternary
+//    matrices scatter +v into the positive key's bin and -v into the negative
+//    key's bin of ONE histogram: the fold is linear, so fold(u+ - u-) equals
+//    the reference's `pos - neg` (kernels.py:206) exactly in integer arithmetic.
+//    One warp folds the finished histogram (RSR++ pairwise compaction,
+//    kernels.py:74-91, or the dense RSR product, kernels.py:63-71) while the
+//    other warps already scatter the next block into the second buffer.
+//
+//  * GATHER (fp32 / fp64 / deterministic int32) — the paper's Eq. 4 form
+//    (`_segment_sums`, kernels.py:50-60): u[j] = sum over sorted positions
+//    p in [seg[j], seg[j+1]) of v[perm[p]].  v is staged in shared memory; one
+//    warp streams a block's perm in 256-position windows (8 positions per lane,
+//    one 16-byte load), gathers v, and computes window-local prefix sums with a
+//    warp-shuffle scan.  Each bucket boundary then contributes its window-local
+//    prefix with the RSR++ telescoping coefficients (bit_s(j-1) - bit_s(j)),
+//    i.e. the pairwise compaction of Alg. 3 applied to prefix sums (about two
+//    adds per bucket), or — for variant "rsr" — the segment sum u_j is formed
+//    and added to every column whose bit is set (w adds per bucket).  No
+//    floating-point atomics: results are deterministic run to run.
+#include "common.cuh"
+
+namespace rsr {
+
+namespace {
+
+constexpr int kScatterThreads = 1024;
+constexpr int kMaxK = 16;
+constexpr int kRegFoldMaxK = 11;  // RSR++ register fold handles <= 2^11 bins; larger k folds top bits in smem
+
+// =====================================================================================
+// fold of one 2^K-bin int32 histogram by one warp -> r_s (s = LSB shift) in lane s.
+// Zeroes the histogram as it reads it.
+// =====================================================================================
+
+__device__ __forceinline__ int32_t keep_if(int lane, int s, int32_t val) { return lane == s ? val : 0; }
+
+// RSR++: pairwise compaction (kernels.py:74-91).  Bits above kRegFoldMaxK are folded
+// first in shared memory from the top (r_top = sum of the upper half, u' = lower + upper),
+// the remaining <= 2^11 bins are folded in registers.
+__device__ int32_t fold_rsrpp_warp(int32_t* __restrict__ H, int K, int lane) {
+  int32_t mine = 0;
+  int Kc = K;
+  while (Kc > kRegFoldMaxK) {
+    const int half4 = 1 << (Kc - 3);  // int4 count of the lower half
+    int4* H4 = reinterpret_cast<int4*>(H);
+    int32_t acc = 0;
+    for (int q = lane; q < half4; q += 32) {
+      int4 a = H4[q], c = H4[q + half4];
+      acc += (c.x + c.y) + (c.z + c.w);
+      H4[q] = make_int4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
+      H4[q + half4] = make_int4(0, 0, 0, 0);
+    }
+    mine += keep_if(lane, Kc - 1, warp_sum(acc));
+    --Kc;
+    __syncwarp();
+  }
+  if (Kc >= 7) {
+    // bins j = 4*(lane + 32*i) + e : bits 0-1 = e (local), bits 2-6 = lane, bits 7.. = i (local)
+    const int ni = 1 << (Kc - 7);
+    int4* H4 = reinterpret_cast<int4*>(H);
+    int32_t z[16];
+    int32_t p0 = 0, p1 = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < ni) {
+        int4 q = H4[lane + 32 * i];
+        H4[lane + 32 * i] = make_int4(0, 0, 0, 0);
+        p0 += q.y + q.w;
+        int32_t y0 = q.x + q.y, y1 = q.z + q.w;
+        p1 += y1;
+        z[i] = y0 + y1;
+      } else {
+        z[i] = 0;
+      }
+    }
+    mine += keep_if(lane, 0, warp_sum(p0));
+    mine += keep_if(lane, 1, warp_sum(p1));
+    // local i bits -> global bits 7..Kc-1
+#pragma unroll
+    for (int L = 0; L < 4; ++L) {
+      if (7 + L < Kc) {
+        const int cnt = ni >> (L + 1);
+        int32_t odd = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t < cnt) {
+            odd += z[2 * t + 1];
+            z[t] = z[2 * t] + z[2 * t + 1];
+          }
+        }
+        mine += keep_if(lane, 7 + L, warp_sum(odd));
+      }
+    }
+    const int32_t X = z[0];
+#pragma unroll
+    for (int s = 2; s < 7; ++s) mine += keep_if(lane, s, warp_sum(((lane >> (s - 2)) & 1) ? X : 0));
+  } else {
+    // scalar layout for <= 64 bins: bits 0-4 = lane, bit 5 = local
+    const int nb = 1 << Kc;
+    int32_t x0 = lane < nb ? H[lane] : 0;
+    int32_t x1 = (nb == 64) ? H[lane + 32] : 0;
+    if (lane < nb) H[lane] = 0;
+    if (nb == 64) H[lane + 32] = 0;
+    if (Kc == 6) mine += keep_if(lane, 5, warp_sum(x1));
+    const int32_t X = x0 + x1;
+    const int lb = Kc < 5 ? Kc : 5;
+    for (int s = 0; s < lb; ++s) mine += keep_if(lane, s, warp_sum(((lane >> s) & 1) ? X : 0));
+  }
+  return mine;
+}
+
+// RSR: dense block product r_s = sum_j u[j] * bit_s(j) (kernels.py:63-71), K*2^K adds.
+__device__ int32_t fold_rsr_warp(int32_t* __restrict__ H, int K, int lane) {
+  int32_t acc[kMaxK];
+#pragma unroll
+  for (int s = 0; s < kMaxK; ++s) acc[s] = 0;
+  const int nb = 1 << K;
+  for (int j = lane; j < nb; j += 32) {
+    const int32_t u = H[j];
+    H[j] = 0;
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s)
+      if (s < K) acc[s] += ((j >> s) & 1) ? u : 0;
+  }
+  int32_t mine = 0;
+#pragma unroll
+  for (int s = 0; s < kMaxK; ++s)
+    if (s < K) mine += keep_if(lane, s, warp_sum(acc[s]));
+  return mine;
+}
+
+// =====================================================================================
+// SCATTER kernel (int32)
+// =====================================================================================
+
+struct ScatterParams {
+  const uint16_t* key[2];
+  const int32_t* v;
+  void* out;
+  int64_t rows, cols, row_stride;
+  int k, halves, b_begin, b_end;
+  int rows_per_cta, n_splits, stages, atomic_out, nhist;
+};
+
+template <typename OutT>
+__device__ __forceinline__ void emit(OutT* out, int64_t col, int32_t val, bool atomic) {
+  if (atomic) atomicAdd(out + col, (OutT)val);
+  else out[col] = (OutT)val;
+}
+
+template <int R, bool FOLDPP, typename OutT>
+__global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const ScatterParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int T = blockDim.x;
+  const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  const int nbk = 1 << p.k;
+  const int rpc = p.rows_per_cta;
+  const int S = p.stages;
+  int32_t* hist = reinterpret_cast<int32_t*>(smem);
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + sizeof(int32_t) * p.nhist * nbk);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)S * p.halves * rpc);
+
+  const int split = blockIdx.x % p.n_splits;
+  const int col_cta = blockIdx.x / p.n_splits;
+  const int ncol = gridDim.x / p.n_splits;
+  const int64_t r0 = (int64_t)split * rpc;
+  const int nblk = p.b_end - p.b_begin;
+  const int nunits = col_cta < nblk ? (nblk - col_cta + ncol - 1) / ncol : 0;
+  const int rows_copy = (int)std::min<int64_t>(rpc, p.row_stride - r0);  // multiple of 8
+  const uint32_t copy_bytes = (uint32_t)rows_copy * 2u;
+  const int rows_valid = (int)std::min<int64_t>(rpc, p.rows - r0);
+  const uint16_t* key0 = p.key[0];
+  const uint16_t* key1 = p.key[1];
+
+  // zero both histograms and the never-copied tail of every ring slot
+  for (int i = t; i < p.nhist * nbk; i += T) hist[i] = 0;
+  for (int sl = 0; sl < S * p.halves; ++sl)
+    for (int i = rows_copy + t; i < rpc; i += T) ring[(size_t)sl * rpc + i] = 0;
+
+  // this CTA's slice of v lives in registers for the whole launch
+  int32_t vr[R];
+#pragma unroll
+  for (int g = 0; g < R / 8; ++g) {
+    const int lr = 8 * (t + T * g);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) vr[g * 8 + e] = (lr + e < rows_valid) ? p.v[r0 + lr + e] : 0;
+  }
+
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint64_t policy = 0;
+  if (t == 0) {
+    policy = l2_evict_first_policy();
+    for (int u = 0; u < S && u < nunits; ++u) {
+      const int b = p.b_begin + col_cta + u * ncol;
+      mbar_arrive_expect_tx(&bars[u], copy_bytes * p.halves);
+      for (int h = 0; h < p.halves; ++h)
+        tma_load_1d(ring + ((size_t)u * p.halves + h) * rpc, (h ? key1 : key0) + (int64_t)b * p.row_stride + r0, copy_bytes,
+                    &bars[u], policy);
+    }
+  }
+
+  OutT* out = reinterpret_cast<OutT*>(p.out);
+  for (int u = 0; u < nunits; ++u) {
+    const int stage = u % S;
+    const int b = p.b_begin + col_cta + u * ncol;
+    int32_t* H = hist + (p.nhist == 2 ? (u & 1) * nbk : 0);
+    mbar_wait(&bars[stage], (uint32_t)((u / S) & 1));
+    for (int h = 0; h < p.halves; ++h) {
+      const uint4* kk = reinterpret_cast<const uint4*>(ring + ((size_t)stage * p.halves + h) * rpc);
+#pragma unroll
+      for (int g = 0; g < R / 8; ++g) {
+        if (8 * (t + T * g) < rows_valid) {
+          const uint4 q = kk[t + T * g];
+          const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
+            atomicAdd(&H[w4[e] & 0xffffu], h ? -a : a);
+            atomicAdd(&H[w4[e] >> 16], h ? -c : c);
+          }
+        }
+      }
+    }
+    __syncthreads();  // histogram complete, ring slot consumed
+    if (t == 0 && u + S < nunits) {
+      const int bn = p.b_begin + col_cta + (u + S) * ncol;
+      mbar_arrive_expect_tx(&bars[stage], copy_bytes * p.halves);
+      for (int h = 0; h < p.halves; ++h)
+        tma_load_1d(ring + ((size_t)stage * p.halves + h) * rpc, (h ? key1 : key0) + (int64_t)bn * p.row_stride + r0,
+                    copy_bytes, &bars[stage], policy);
+    }
+    if (warp == (u & 31) % (T >> 5)) {
+      const int32_t r = FOLDPP ? fold_rsrpp_warp(H, p.k, lane) : fold_rsr_warp(H, p.k, lane);
+      const int w = block_width(p.cols, p.k, b);
+      if (lane < w) emit(out, (int64_t)b * p.k + (w - 1 - lane), r, p.atomic_out != 0);
+    }
+    if (p.nhist == 1) __syncthreads();  // single histogram: zeroed before the next scatter
+  }
+}
+
+// =====================================================================================
+// GATHER kernel (fp32 / fp64 / int32)
+// =====================================================================================
+
+struct GatherParams {
+  const void* perm[2];
+  const uint32_t* seg[2];
+  const void* v;
+  void* out;
+  int64_t rows, cols, row_stride, seg_stride;
+  int k, halves, b_begin, b_end;
+  int perm_bytes, v_in_smem, warps_per_cta;
+};
+
+template <typename T>
+__device__ __forceinline__ T vload(const T* vs, const T* vg, uint32_t row, bool smem) {
+  return smem ? vs[row] : __ldg(vg + row);
+}
+
+template <typename T, bool FOLDPP>
+__global__ void __launch_bounds__(512) gather_kernel(const GatherParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  T* pbuf_all = reinterpret_cast<T*>(smem);
+  T* pbuf = pbuf_all + wib * 256;
+  T* vs = pbuf_all + p.warps_per_cta * 256;
+  const T* vg = reinterpret_cast<const T*>(p.v);
+  const bool vsm = p.v_in_smem != 0;
+  if (vsm) {
+    const int64_t n = p.rows;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) vs[i] = vg[i];
+    __syncthreads();
+  }
+  const int nwarps_total = gridDim.x * p.warps_per_cta;
+  const int gw = blockIdx.x * p.warps_per_cta + wib;
+  T* out = reinterpret_cast<T*>(p.out);
+  const uint32_t* seg0 = p.seg[0];
+  const uint32_t* seg1 = p.seg[1];
+  const void* perm0 = p.perm[0];
+  const void* perm1 = p.perm[1];
+
+  for (int b = p.b_begin + gw; b < p.b_end; b += nwarps_total) {
+    const int w = block_width(p.cols, p.k, b);
+    const int nbk = 1 << w;
+    T acc[kMaxK];
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s) acc[s] = T(0);
+    for (int h = 0; h < p.halves; ++h) {
+      const T sgn = h ? T(-1) : T(1);
+      const uint32_t* seg = (h ? seg1 : seg0) + (int64_t)b * p.seg_stride;
+      const void* permh = h ? perm1 : perm0;
+      const uint16_t* perm16 = reinterpret_cast<const uint16_t*>(permh) + (int64_t)b * p.row_stride;
+      const uint32_t* perm32 = reinterpret_cast<const uint32_t*>(permh) + (int64_t)b * p.row_stride;
+      int jcur = 1;      // next boundary to consume (boundary j sits at position seg[j])
+      T carry = T(0);    // RSR: partial sum of the bucket open at the window start
+      for (int64_t w0 = 0; w0 < p.rows; w0 += 256) {
+        const int E = (int)std::min<int64_t>(256, p.rows - w0);
+        const int64_t pos0 = w0 + 8 * lane;
+        uint32_t rowsel[8];
+        if (p.perm_bytes == 2) {
+          uint4 q = make_uint4(0, 0, 0, 0);
+          if (pos0 < p.row_stride) q = ld_nc_v4(perm16 + pos0);
+          rowsel[0] = q.x & 0xffffu; rowsel[1] = q.x >> 16;
+          rowsel[2] = q.y & 0xffffu; rowsel[3] = q.y >> 16;
+          rowsel[4] = q.z & 0xffffu; rowsel[5] = q.z >> 16;
+          rowsel[6] = q.w & 0xffffu; rowsel[7] = q.w >> 16;
+        } else {
+          uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+          if (pos0 < p.row_stride) { q0 = ld_nc_v4(perm32 + pos0); q1 = ld_nc_v4(perm32 + pos0 + 4); }
+          rowsel[0] = q0.x; rowsel[1] = q0.y; rowsel[2] = q0.z; rowsel[3] = q0.w;
+          rowsel[4] = q1.x; rowsel[5] = q1.y; rowsel[6] = q1.z; rowsel[7] = q1.w;
+        }
+        T x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = (pos0 + e < p.rows) ? vload(vs, vg, rowsel[e], vsm) : T(0);
+#pragma unroll
+        for (int e = 1; e < 8; ++e) x[e] += x[e - 1];
+        const T incl = warp_inclusive_scan(x[7], lane);
+        const T base = incl - x[7];
+        const T total = __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pbuf[8 * lane + e] = base + x[e];
+        __syncwarp();
+        // consume the boundaries that fall in (w0, w0 + E] (window 0: [0, E])
+        int last_in = -1;  // lane index of the last included boundary in the final batch
+        T p_last = T(0);
+        while (true) {
+          const int jj = jcur + lane;
+          const int64_t sj = jj <= nbk ? (int64_t)seg[jj] : INT64_MAX;
+          const bool in = sj <= w0 + E;
+          const unsigned bal = __ballot_sync(0xffffffffu, in);
+          const int cnt = __popc(bal);
+          T P = T(0);
+          if (in) {
+            const int q = (int)(sj - w0);
+            P = q ? pbuf[q - 1] : T(0);
+          }
+          if (FOLDPP) {
+            if (in) {
+              // boundary j closes bucket j-1 and opens bucket j: coefficient bit_s(j-1) - bit_s(j)
+              const int tz = __ffs(jj) - 1;
+#pragma unroll
+              for (int s = 0; s < kMaxK; ++s) acc[s] += (s < tz) ? sgn * P : ((s == tz) ? -sgn * P : T(0));
+            }
+          } else {
+            // segment sum of bucket jj-1 = P(jj) - P(previous boundary) (+ carry for the first)
+            T prevP = __shfl_up_sync(0xffffffffu, P, 1);
+            if (in) {
+              const T uj = (lane == 0) ? carry + P : P - prevP;
+              const int j = jj - 1;
+#pragma unroll
+              for (int s = 0; s < kMaxK; ++s) acc[s] += ((j >> s) & 1) ? sgn * uj : T(0);
+            }
+            if (cnt > 0) {
+              p_last = __shfl_sync(0xffffffffu, P, cnt - 1);
+              carry = T(0);
+              last_in = cnt - 1;
+            }
+          }
+          jcur += cnt;
+          if (cnt < 32) break;
+          if (!FOLDPP) carry = T(0) - p_last;  // next batch's first boundary continues from p_last
+        }
+        if (FOLDPP) {
+          // bucket open at the window end contributes the whole window tail: bit_s(g) * total
+          const int g = jcur - 1;
+          if (lane == 0) {
+#pragma unroll
+            for (int s = 0; s < kMaxK; ++s) acc[s] += ((g >> s) & 1) ? sgn * total : T(0);
+          }
+        } else {
+          carry = (last_in >= 0) ? total - p_last : carry + total;
+        }
+        __syncwarp();
+      }
+    }
+    // reduce the per-lane column accumulators; lane s writes column w-1-s
+    T mine = T(0);
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s) {
+      if (s < w) {
+        T r = warp_sum(acc[s]);
+        if (lane == s) mine = r;
+      }
+    }
+    if (lane < w) out[(int64_t)b * p.k + (w - 1 - lane)] = mine;
+  }
+}
+
+// gather-form bucket sums of one block (segmented_sum, kernels.py:50-60, 94-101):
+// one warp per bucket chunk, ascending-position accumulation per bucket.
+template <typename T>
+__global__ void segmented_sum_kernel(const void* perm, int perm_bytes, const uint32_t* seg, const T* v, int nbk,
+                                     T* u) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nbk) return;
+  const uint32_t lo = seg[j], hi = seg[j + 1];
+  T acc = T(0);
+  for (uint32_t q = lo; q < hi; ++q) {
+    const uint32_t r = perm_bytes == 2 ? reinterpret_cast<const uint16_t*>(perm)[q]
+                                       : reinterpret_cast<const uint32_t*>(perm)[q];
+    acc += v[r];
+  }
+  u[j] = acc;
+}
+
+// Block products of one SegmentedSums vector (block_product_rsr / block_product_rsrpp,
+// kernels.py:104-116): a single thread replays the reference loops in fp64 so the
+// result is bitwise the reference's.  Utility op; the multiply kernels fold in-warp.
+__global__ void block_product_kernel(const double* __restrict__ u, int w, int use_fold, double* __restrict__ buf,
+                                     double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int64_t nseg = (int64_t)1 << w;
+  if (use_fold) {  // kernels.py:74-91
+    int64_t half = nseg >> 1;
+    double acc = 0.0;
+    for (int64_t t = 0; t < half; ++t) {
+      acc += u[2 * t + 1];
+      buf[t] = u[2 * t] + u[2 * t + 1];
+    }
+    out[w - 1] = acc;
+    int64_t size = half;
+    for (int c = w - 2; c >= 0; --c) {
+      half = size >> 1;
+      acc = 0.0;
+      for (int64_t t = 0; t < half; ++t) {
+        acc += buf[2 * t + 1];
+        buf[t] = buf[2 * t] + buf[2 * t + 1];
+      }
+      out[c] = acc;
+      size = half;
+    }
+  } else {  // kernels.py:63-71
+    for (int c = 0; c < w; ++c) {
+      const int shift = w - 1 - c;
+      double acc = 0.0;
+      for (int64_t j = 0; j < nseg; ++j) acc += u[j] * (double)((j >> shift) & 1);
+      out[c] = acc;
+    }
+  }
+}
+
+// Standard dense multiply (core.py:135-169) on the GPU: thread per column, rows ascending.
+template <typename T>
+__global__ void naive_ternary_kernel(const int8_t* __restrict__ A, int64_t rows, int64_t cols, int64_t lda,
+                                     const T* __restrict__ v, T* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  T acc = T(0);
+  for (int64_t i = 0; i < rows; ++i) {
+    const int8_t a = A[i * lda + j];
+    acc += (a == 1) ? v[i] : ((a == -1) ? -v[i] : T(0));
+  }
+  out[j] = acc;
+}
+
+// ------------------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------------------
+
+template <int R, bool PP, typename OutT>
+rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
+  auto kern = scatter_kernel<R, PP, OutT>;
+  rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                             "scatter smem attribute");
+  if (st != RSR_OK) return st;
+  kern<<<grid, threads, smem, s>>>(p);
+  return cuda_check(cudaGetLastError(), "scatter_kernel launch");
+}
+
+template <int R, typename OutT>
+rsr_status launch_scatter_r(const ScatterParams& p, bool pp, int grid, size_t smem, int threads, cudaStream_t s) {
+  return pp ? launch_scatter_t<R, true, OutT>(p, grid, smem, threads, s)
+            : launch_scatter_t<R, false, OutT>(p, grid, smem, threads, s);
+}
+
+rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out, rsr_dtype out_dtype, bool pp,
+                            int b0, int b1, cudaStream_t s) {
+  if (d.k > 15) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply supports k <= 15");
+  ScatterParams p{};
+  for (int h = 0; h < d.halves; ++h) p.key[h] = d.half[h].bucket;
+  p.v = v;
+  p.out = out;
+  p.rows = d.rows;
+  p.cols = d.cols;
+  p.row_stride = d.row_stride;
+  p.k = d.k;
+  p.halves = d.halves;
+  p.b_begin = b0;
+  p.b_end = b1;
+  // rows per thread R (8 or 16), threads per CTA, row splits
+  const int R = d.rows > 8192 ? 16 : 8;
+  int threads = kScatterThreads;
+  if (d.rows <= (int64_t)R * kScatterThreads) {
+    const int64_t need = (d.rows + R - 1) / R;
+    threads = (int)std::max<int64_t>(32, ((need + 31) / 32) * 32);
+  }
+  p.rows_per_cta = threads * R;
+  p.n_splits = (int)((d.rows + p.rows_per_cta - 1) / p.rows_per_cta);
+  p.atomic_out = p.n_splits > 1;
+  const size_t slot_bytes = (size_t)d.halves * p.rows_per_cta * 2;
+  const size_t max_smem = device_max_smem_optin();
+  // double-buffered histograms when they fit next to >= 2 ring stages, else one
+  p.nhist = (sizeof(int32_t) * 2 * ((size_t)1 << d.k) + 2 * slot_bytes + 256 <= max_smem) ? 2 : 1;
+  const size_t hist_bytes = sizeof(int32_t) * p.nhist * ((size_t)1 << d.k);
+  int stages = 4;
+  while (stages > 1 && hist_bytes + stages * slot_bytes + 8 * stages + 128 > max_smem) --stages;
+  if (hist_bytes + stages * slot_bytes + 8 * stages + 128 > max_smem)
+    return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: index slice does not fit in shared memory");
+  p.stages = stages;
+  const size_t smem = hist_bytes + stages * slot_bytes + 8 * stages;
+  const int nblk = b1 - b0;
+  const int sms = device_sm_count();
+  int ncol = std::max(1, std::min(nblk, sms / std::max(1, p.n_splits)));
+  if (ncol < 1) ncol = 1;
+  const int grid = ncol * p.n_splits;
+  if (p.atomic_out) {
+    const size_t esz = out_dtype == RSR_F64 ? 8 : 4;
+    const int64_t c0 = (int64_t)b0 * d.k;
+    const int64_t c1 = std::min<int64_t>(d.cols, (int64_t)b1 * d.k);
+    rsr_status st = cuda_check(cudaMemsetAsync((char*)out + c0 * esz, 0, (c1 - c0) * esz, s), "memset out");
+    if (st != RSR_OK) return st;
+  }
+  if (out_dtype == RSR_F64)
+    return R == 16 ? launch_scatter_r<16, double>(p, pp, grid, smem, threads, s)
+                   : launch_scatter_r<8, double>(p, pp, grid, smem, threads, s);
+  return R == 16 ? launch_scatter_r<16, int32_t>(p, pp, grid, smem, threads, s)
+                 : launch_scatter_r<8, int32_t>(p, pp, grid, smem, threads, s);
+}
+
+template <typename T>
+rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, bool pp, int b0, int b1,
+                             cudaStream_t s) {
+  GatherParams p{};
+  for (int h = 0; h < d.halves; ++h) {
+    p.perm[h] = d.half[h].perm;
+    p.seg[h] = d.half[h].seg;
+  }
+  p.v = v;
+  p.out = out;
+  p.rows = d.rows;
+  p.cols = d.cols;
+  p.row_stride = d.row_stride;
+  p.seg_stride = d.seg_stride;
+  p.k = d.k;
+  p.halves = d.halves;
+  p.b_begin = b0;
+  p.b_end = b1;
+  p.perm_bytes = d.perm_bytes;
+  const size_t max_smem = device_max_smem_optin();
+  const int nblk = b1 - b0;
+  int wpc = 16;
+  const size_t vbytes = sizeof(T) * (size_t)d.rows;
+  p.v_in_smem = (vbytes + sizeof(T) * 256 * wpc) <= max_smem;
+  p.warps_per_cta = wpc;
+  const size_t smem = sizeof(T) * 256 * wpc + (p.v_in_smem ? vbytes : 0);
+  const int ctas_per_sm = p.v_in_smem ? std::max<int>(1, (int)std::min<size_t>(4, (228u << 10) / (smem + 1024))) : 2;
+  const int want = (nblk + wpc - 1) / wpc;
+  const int grid = std::max(1, std::min(want, device_sm_count() * ctas_per_sm));
+  auto kern = pp ? gather_kernel<T, true> : gather_kernel<T, false>;
+  rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                             "gather smem attribute");
+  if (st != RSR_OK) return st;
+  kern<<<grid, 32 * wpc, smem, s>>>(p);
+  return cuda_check(cudaGetLastError(), "gather_kernel launch");
+}
+
+}  // namespace
+
+rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
+                    rsr_form form, int b0, int b1, cudaStream_t s) {
+  const bool pp = var == RSR_VARIANT_RSRPP;
+  if (b0 >= b1) return RSR_OK;
+  if (form == RSR_FORM_AUTO) form = vt == RSR_I32 ? RSR_FORM_SCATTER : RSR_FORM_GATHER;
+  if (form == RSR_FORM_SCATTER) {
+    if (vt != RSR_I32) return fail(RSR_ERR_INVALID, "scatter form needs int32 activations");
+    if (ot != RSR_I32 && ot != RSR_F64) return fail(RSR_ERR_INVALID, "int32 activations produce int32 or float64");
+    return multiply_scatter(d, (const int32_t*)v, out, ot, pp, b0, b1, s);
+  }
+  if (vt != ot) return fail(RSR_ERR_INVALID, "gather form writes the activation dtype");
+  switch (vt) {
+    case RSR_I32: return multiply_gather_t<int32_t>(d, v, out, pp, b0, b1, s);
+    case RSR_F32: return multiply_gather_t<float>(d, v, out, pp, b0, b1, s);
+    case RSR_F64: return multiply_gather_t<double>(d, v, out, pp, b0, b1, s);
+  }
+  return fail(RSR_ERR_INVALID, "unknown dtype");
+}
+
+rsr_status segmented_sum(const rsr_index_desc& d, int half, int block, const void* v, rsr_dtype dt, void* u,
+                         cudaStream_t s) {
+  const int w = block_width(d.cols, d.k, block);
+  const int nbk = 1 << w;
+  const void* perm = (const char*)d.half[half].perm + (size_t)block * d.row_stride * d.perm_bytes;
+  const uint32_t* seg = d.half[half].seg + (size_t)block * d.seg_stride;
+  const int grid = (nbk + 255) / 256;
+  switch (dt) {
+    case RSR_I32: segmented_sum_kernel<int32_t><<<grid, 256, 0, s>>>(perm, d.perm_bytes, seg, (const int32_t*)v, nbk, (int32_t*)u); break;
+    case RSR_F32: segmented_sum_kernel<float><<<grid, 256, 0, s>>>(perm, d.perm_bytes, seg, (const float*)v, nbk, (float*)u); break;
+    case RSR_F64: segmented_sum_kernel<double><<<grid, 256, 0, s>>>(perm, d.perm_bytes, seg, (const double*)v, nbk, (double*)u); break;
+  }
+  return cuda_check(cudaGetLastError(), "segmented_sum_kernel launch");
+}
+
+rsr_status block_product(const double* u, int w, int use_fold, double* buf, double* out, cudaStream_t s) {
+  block_product_kernel<<<1, 32, 0, s>>>(u, w, use_fold, buf, out);
+  return cuda_check(cudaGetLastError(), "block_product_kernel launch");
+}
+
+rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t lda, const void* v, rsr_dtype dt,
+                         void* out, cudaStream_t s) {
+  const unsigned grid = (unsigned)((cols + 255) / 256);
+  switch (dt) {
+    case RSR_I32: naive_ternary_kernel<int32_t><<<grid, 256, 0, s>>>(A, rows, cols, lda, (const int32_t*)v, (int32_t*)out); break;
+    case RSR_F32: naive_ternary_kernel<float><<<grid, 256, 0, s>>>(A, rows, cols, lda, (const float*)v, (float*)out); break;
+    case RSR_F64: naive_ternary_kernel<double><<<grid, 256, 0, s>>>(A, rows, cols, lda, (const double*)v, (double*)out); break;
+  }
+  return cuda_check(cudaGetLastError(), "naive_ternary_kernel launch");
+}
+
+}  // namespace rsr

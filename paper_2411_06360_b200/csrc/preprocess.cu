@@ -1,0 +1,224 @@
+// GPU preprocessing: ternary/binary matrix -> per-block keys -> stable counting
+// sort (perm) + cumulative segmentation (seg).
+//
+// Reference algorithm (indexer.py:251-286, core.py:124-128):
+//   for each half (A == +1, A == -1) and each column block of width w:
+//     key(r)  = MSB-first bits of row r inside the block            (indexer.py:215-219)
+//     perm    = np.argsort(key, kind="stable")                       (indexer.py:269)
+//     seg     = [0, cumsum(bincount(key, minlength=2^w))]            (indexer.py:274-276)
+// B200 design: one kernel turns the int8 matrix into both halves' keys for all
+// blocks (smem-tiled so global reads and key writes are coalesced); a second
+// kernel gives each (half, block) to one warp, which builds the histogram in a
+// warp-private shared-memory counter array, scans it into `seg`, and then walks
+// the rows in ascending order 32 at a time, ranking equal keys with
+// __match_any_sync so the scatter into `perm` is stable by construction.
+#include "common.cuh"
+
+namespace rsr {
+
+namespace {
+
+constexpr int kKeyRowsPerTile = 64;
+constexpr int kKeyThreads = 256;
+constexpr int kKeyTileBytes = 512;  // max columns per tile
+
+// Grid: x = row tiles, y = block tiles.  Each block tile holds `bt` column blocks.
+__global__ void __launch_bounds__(kKeyThreads) keys_ternary_kernel(const int8_t* __restrict__ A, int64_t lda,
+                                                                     int64_t rows, int64_t cols, int k, int bt,
+                                                                     int64_t row_stride, uint16_t* __restrict__ kpos,
+                                                                     uint16_t* __restrict__ kneg,
+                                                                     int32_t* __restrict__ bad) {
+  // Row pitch: an odd number of 4-byte words keeps the per-lane row accesses on distinct banks.
+  __shared__ int8_t tile[kKeyRowsPerTile * (kKeyTileBytes + 4)];
+  const int pitch = kKeyTileBytes + 4;
+  const int64_t r0 = (int64_t)blockIdx.x * kKeyRowsPerTile;
+  const int b0 = blockIdx.y * bt;
+  const int64_t c0 = (int64_t)b0 * k;
+  const int tw = (int)std::min<int64_t>((int64_t)bt * k, cols - c0);
+  const int nr = (int)std::min<int64_t>(kKeyRowsPerTile, rows - r0);
+  int nbad = 0;
+  for (int idx = threadIdx.x; idx < nr * tw; idx += kKeyThreads) {
+    int r = idx / tw, c = idx - r * tw;
+    int8_t x = A[(r0 + r) * lda + c0 + c];
+    nbad += (x < -1 || x > 1);
+    tile[r * pitch + c] = x;
+  }
+  if (nbad) atomicAdd(bad, nbad);
+  __syncthreads();
+  const int nblk = (tw + k - 1) / k;
+  for (int p = threadIdx.x; p < kKeyRowsPerTile * nblk; p += kKeyThreads) {
+    int r = p % kKeyRowsPerTile, bl = p / kKeyRowsPerTile;
+    if (r >= nr) continue;
+    int w = min(k, tw - bl * k);
+    const int8_t* src = tile + r * pitch + bl * k;
+    unsigned kp = 0, kn = 0;
+    for (int c = 0; c < w; ++c) {
+      int8_t x = src[c];
+      kp = (kp << 1) | (unsigned)(x == 1);
+      kn = (kn << 1) | (unsigned)(x == -1);
+    }
+    int64_t o = (int64_t)(b0 + bl) * row_stride + r0 + r;
+    kpos[o] = (uint16_t)kp;
+    kneg[o] = (uint16_t)kn;
+  }
+}
+
+// BinaryMatrix bits (core.py:53-99): row-major bytes, MSB-first within a byte.
+__global__ void keys_binary_kernel(const uint8_t* __restrict__ bits, int64_t ldb, int64_t rows, int64_t cols, int k,
+                                   int nblocks, int64_t row_stride, uint16_t* __restrict__ keys) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const uint8_t* row = bits + r * ldb;
+  for (int b = blockIdx.y; b < nblocks; b += gridDim.y) {
+    int w = block_width(cols, k, b);
+    int64_t c0 = (int64_t)b * k;
+    unsigned key = 0;
+    for (int c = 0; c < w; ++c) {
+      int64_t cc = c0 + c;
+      key = (key << 1) | ((row[cc >> 3] >> (7 - (cc & 7))) & 1u);
+    }
+    keys[(int64_t)b * row_stride + r] = (uint16_t)key;
+  }
+}
+
+// One warp per (half, block): histogram -> exclusive scan (seg) -> stable ranked scatter (perm).
+template <typename PermT>
+__global__ void sort_blocks_kernel(rsr_index_desc d, uint32_t* __restrict__ gcnt, int use_smem, int warps_per_cta) {
+  extern __shared__ uint32_t scnt[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t unit = (int64_t)blockIdx.x * warps_per_cta + wib;  // (half, block)
+  const int64_t nunits = (int64_t)d.halves * d.nblocks;
+  if (unit >= nunits) return;
+  const int h = (int)(unit / d.nblocks);
+  const int b = (int)(unit % d.nblocks);
+  const int w = block_width(d.cols, d.k, b);
+  const int nbk = 1 << w;
+  uint32_t* cnt = use_smem ? scnt + ((size_t)wib << d.k) : gcnt + ((size_t)unit << d.k);
+  const uint16_t* key = d.half[h].bucket + (int64_t)b * d.row_stride;
+  uint32_t* seg = d.half[h].seg + (int64_t)b * d.seg_stride;
+  PermT* perm = reinterpret_cast<PermT*>(d.half[h].perm) + (int64_t)b * d.row_stride;
+  const int64_t rows = d.rows;
+
+  for (int j = lane; j < nbk; j += 32) cnt[j] = 0;
+  __syncwarp();
+  for (int64_t r = lane; r < rows; r += 32) atomicAdd(&cnt[key[r]], 1u);
+  __syncwarp();
+  // Exclusive scan of cnt[0..nbk): lane owns a contiguous chunk.
+  const int chunk = (nbk + 31) / 32;
+  const int j0 = min(nbk, lane * chunk), j1 = min(nbk, j0 + chunk);
+  uint32_t local = 0;
+  for (int j = j0; j < j1; ++j) local += cnt[j];
+  uint32_t incl = warp_inclusive_scan(local, lane);
+  uint32_t run = incl - local;
+  for (int j = j0; j < j1; ++j) {
+    uint32_t c = cnt[j];
+    seg[j] = run;
+    cnt[j] = run;  // becomes the per-key write cursor
+    run += c;
+  }
+  for (int64_t j = nbk + lane; j < d.seg_stride; j += 32) seg[j] = (uint32_t)rows;  // sentinel (+ unused tail)
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t r0 = 0; r0 < rows; r0 += 32) {
+    const int64_t r = r0 + lane;
+    const bool active = r < rows;
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (active) {
+      const unsigned kk = key[r];
+      const unsigned peers = __match_any_sync(act, kk);
+      const int leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (lane == leader) {
+        base = cnt[kk];
+        cnt[kk] = base + __popc(peers);
+      }
+      base = __shfl_sync(act, base, leader);
+      perm[base + __popc(peers & lt)] = (PermT)r;
+    }
+    __syncwarp();
+  }
+}
+
+rsr_status launch_sort(const rsr_index_desc& d, void* workspace, size_t ws_bytes, cudaStream_t s) {
+  const size_t per_warp = sizeof(uint32_t) << d.k;
+  const int64_t nunits = (int64_t)d.halves * d.nblocks;
+  int wpc = (int)std::min<size_t>(8, (160u << 10) / per_warp);
+  const bool use_smem = wpc >= 1;
+  if (!use_smem) {
+    wpc = 8;
+    if (ws_bytes < per_warp * (size_t)nunits) return fail(RSR_ERR_INVALID, "preprocess workspace too small");
+  }
+  const size_t smem = use_smem ? per_warp * wpc : 0;
+  const unsigned grid = (unsigned)((nunits + wpc - 1) / wpc);
+  if (d.perm_bytes == 2) {
+    auto kern = sort_blocks_kernel<uint16_t>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 32 * wpc, smem, s>>>(d, (uint32_t*)workspace, use_smem, wpc);
+  } else {
+    auto kern = sort_blocks_kernel<uint32_t>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 32 * wpc, smem, s>>>(d, (uint32_t*)workspace, use_smem, wpc);
+  }
+  return cuda_check(cudaGetLastError(), "sort_blocks_kernel launch");
+}
+
+rsr_status clear_index(const rsr_index_desc& d, cudaStream_t s) {
+  for (int h = 0; h < d.halves; ++h) {
+    size_t nb = (size_t)d.nblocks * d.row_stride;
+    rsr_status st = cuda_check(cudaMemsetAsync(d.half[h].bucket, 0, nb * 2, s), "memset bucket");
+    if (st != RSR_OK) return st;
+    st = cuda_check(cudaMemsetAsync(d.half[h].perm, 0, nb * d.perm_bytes, s), "memset perm");
+    if (st != RSR_OK) return st;
+  }
+  return RSR_OK;
+}
+
+rsr_status check_desc(const rsr_index_desc* d) {
+  if (!d) return fail(RSR_ERR_INVALID, "null index descriptor");
+  if (d->rows < 1 || d->cols < 1) return fail(RSR_ERR_INVALID, "index dimensions must be at least 1x1");
+  if (d->k < 1 || d->k > kMaxDeviceK) return fail(RSR_ERR_UNSUPPORTED, "k exceeds the device limit of 16");
+  for (int h = 0; h < d->halves; ++h)
+    if (!d->half[h].perm || !d->half[h].seg || !d->half[h].bucket)
+      return fail(RSR_ERR_INVALID, "index descriptor has null arrays");
+  return RSR_OK;
+}
+
+}  // namespace
+
+size_t preprocess_workspace_bytes(const rsr_index_desc* d) {
+  const size_t per_warp = sizeof(uint32_t) << d->k;
+  if ((160u << 10) / per_warp >= 1) return 0;
+  return per_warp * (size_t)d->halves * d->nblocks;
+}
+
+rsr_status preprocess_ternary(const int8_t* A, int64_t lda, const rsr_index_desc* d, int32_t* bad, void* ws,
+                              size_t ws_bytes, cudaStream_t s) {
+  rsr_status st = check_desc(d);
+  if (st != RSR_OK) return st;
+  if (d->halves != 2) return fail(RSR_ERR_INVALID, "ternary preprocess needs a two-half index");
+  if (!A || !bad || lda < d->cols) return fail(RSR_ERR_INVALID, "bad ternary matrix arguments");
+  if ((st = clear_index(*d, s)) != RSR_OK) return st;
+  const int bt = std::max(1, kKeyTileBytes / d->k);
+  dim3 grid((unsigned)((d->rows + kKeyRowsPerTile - 1) / kKeyRowsPerTile), (unsigned)((d->nblocks + bt - 1) / bt));
+  keys_ternary_kernel<<<grid, kKeyThreads, 0, s>>>(A, lda, d->rows, d->cols, d->k, bt, d->row_stride,
+                                                   d->half[0].bucket, d->half[1].bucket, bad);
+  if ((st = cuda_check(cudaGetLastError(), "keys_ternary_kernel launch")) != RSR_OK) return st;
+  return launch_sort(*d, ws, ws_bytes, s);
+}
+
+rsr_status preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_desc* d, void* ws, size_t ws_bytes,
+                             cudaStream_t s) {
+  rsr_status st = check_desc(d);
+  if (st != RSR_OK) return st;
+  if (d->halves != 1) return fail(RSR_ERR_INVALID, "binary preprocess needs a one-half index");
+  if (!bits || ldb < (d->cols + 7) / 8) return fail(RSR_ERR_INVALID, "bad binary matrix arguments");
+  if ((st = clear_index(*d, s)) != RSR_OK) return st;
+  dim3 grid((unsigned)((d->rows + 255) / 256), (unsigned)std::min(d->nblocks, 65535));
+  keys_binary_kernel<<<grid, 256, 0, s>>>(bits, ldb, d->rows, d->cols, d->k, d->nblocks, d->row_stride,
+                                          d->half[0].bucket);
+  if ((st = cuda_check(cudaGetLastError(), "keys_binary_kernel launch")) != RSR_OK) return st;
+  return launch_sort(*d, ws, ws_bytes, s);
+}
+
+}  // namespace rsr

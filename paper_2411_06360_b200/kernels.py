@@ -1,0 +1,259 @@
+"""Inference: segmented sums, block products and the fused multiply, on the GPU.
+
+Mirrors the reference `rsr.kernels` (kernels.py:1-239): same names, argument
+meanings, validation order and error messages.  Every multiply is one launch
+of the sm_100a kernels in librsr_b200.so (see csrc/multiply.cu):
+
+* NumPy / list input keeps the reference contract (fp64 in, fp64 out).  The
+  call copies v to a pinned buffer, and one C-ABI call (`rsr_multiply_host`)
+  does H2D, the multiply and D2H.  fp64 vectors use the deterministic gather
+  kernel in fp64; integer-typed NumPy vectors use the int32 scatter kernel
+  (exact) and still return fp64.
+* torch CUDA tensors stay on the device: int32 -> int32 (scatter kernel, bit-
+  exact), float32 -> float32 and float64 -> float64 (gather kernel).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .core import as_vector
+from .indexer import BlockIndex, RsrIndex, TernaryIndex
+
+_VARIANTS = {"rsr": False, "rsrpp": True, "rsr++": True}
+
+
+def _use_fold(variant: str) -> bool:
+    """kernels.py:17-21."""
+    try:
+        return _VARIANTS[str(variant).lower()]
+    except KeyError:
+        raise ValueError(f"variant must be rsr or rsrpp, got {variant!r}") from None
+
+
+@dataclass(eq=False)
+class SegmentedSums:
+    """Per-bucket sums u of one block; length is exactly 2^width (kernels.py:24-34)."""
+
+    width: int
+    sums: np.ndarray
+
+    def __post_init__(self):
+        self.sums = np.ascontiguousarray(self.sums, np.float64)
+        if self.width < 1 or self.sums.shape != (1 << self.width,):
+            raise ValueError(f"sums length must be 2^{self.width}")
+
+
+def bin_pattern_bit(width: int, row: int, col: int) -> int:
+    """Bit col (0 = most significant) of row's width-bit binary expansion (kernels.py:37-43)."""
+    if not 0 <= row < (1 << width):
+        raise ValueError(f"row {row} out of range for width {width}")
+    if not 0 <= col < width:
+        raise ValueError(f"col {col} out of range for width {width}")
+    return (row >> (width - 1 - col)) & 1
+
+
+# ---------------------------------------------------------------------------
+# per-block operations
+# ---------------------------------------------------------------------------
+
+def segmented_sum(v, block: BlockIndex) -> SegmentedSums:
+    """Per-bucket sums: sums[j] = sum of v[perm[p]] over segment j, ascending p
+    (kernels.py:94-101), computed on the GPU (rsr_segmented_sum)."""
+    import torch
+    v = as_vector(v)
+    if v.shape[0] != block.permutation.shape[0]:
+        raise ValueError(f"vector length {v.shape[0]} does not match {block.permutation.shape[0]} rows")
+    if block._src is not None:
+        idx, b = block._src
+    else:  # a free-standing block: upload it as a one-block index
+        idx = RsrIndex.from_blocks(block.permutation.shape[0], block.width, block.width, [block])
+        b = 0
+    dv = torch.from_numpy(v).cuda()
+    u = torch.empty(1 << block.width, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().rsr_segmented_sum(
+        ctypes.byref(idx.desc), 0, b, dv.data_ptr(), _native.F64, u.data_ptr(), _native.current_stream_ptr()))
+    return SegmentedSums(block.width, u.cpu().numpy())
+
+
+def _block_product(u: SegmentedSums, fold: bool) -> np.ndarray:
+    import torch
+    du = torch.from_numpy(u.sums).cuda()
+    buf = torch.empty(max(1, (1 << u.width) >> 1), dtype=torch.float64, device="cuda")
+    out = torch.empty(u.width, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().rsr_block_product(
+        du.data_ptr(), u.width, _native.VARIANT_RSRPP if fold else _native.VARIANT_RSR,
+        buf.data_ptr(), out.data_ptr(), _native.current_stream_ptr()))
+    return out.cpu().numpy()
+
+
+def block_product_rsr(u: SegmentedSums) -> np.ndarray:
+    """Product of u against the implicit Bin pattern, one column at a time (kernels.py:104-108)."""
+    return _block_product(u, False)
+
+
+def block_product_rsrpp(u: SegmentedSums) -> np.ndarray:
+    """Same value via the odd-sum / pairwise-compaction fold (kernels.py:111-116)."""
+    return _block_product(u, True)
+
+
+# ---------------------------------------------------------------------------
+# fused multiply
+# ---------------------------------------------------------------------------
+
+_DTYPES = {}
+
+
+def _torch_dtype_code(t) -> int:
+    import torch
+    if not _DTYPES:
+        _DTYPES.update({torch.int32: _native.I32, torch.float32: _native.F32, torch.float64: _native.F64})
+    try:
+        return _DTYPES[t.dtype]
+    except KeyError:
+        raise ValueError("device vectors must be int32, float32 or float64") from None
+
+
+class _HostStaging:
+    """Pinned host buffers + device scratch reused by the host-buffer (e2e) path."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, key, shape, dtype, pinned):
+        import torch
+        t = self.bufs.get(key)
+        if t is None or t.numel() < shape or t.dtype != dtype:
+            t = (torch.empty(shape, dtype=dtype, pin_memory=True) if pinned
+                 else torch.empty(shape, dtype=dtype, device="cuda"))
+            self.bufs[key] = t
+        return t[:shape]
+
+
+_staging = _HostStaging()
+
+
+def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO):
+    """Device-tensor path: v CUDA tensor [rows] -> CUDA tensor [cols]."""
+    import torch
+    code = _torch_dtype_code(v)
+    if v.dim() != 1 or v.shape[0] < 1:
+        raise ValueError("vector must be 1-D with at least one entry")
+    if v.shape[0] != idx.rows:
+        raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
+    v = v.contiguous()
+    if out is None:
+        out = torch.empty(idx.cols, dtype=v.dtype, device=v.device)
+    b0, b1 = block_range if block_range is not None else (0, idx.desc.nblocks)
+    _native.check(_native.lib().rsr_multiply(
+        ctypes.byref(idx.desc), v.data_ptr(), code, out.data_ptr(), _torch_dtype_code(out),
+        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, form, b0, b1,
+        _native.current_stream_ptr()))
+    return out
+
+
+def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray:
+    """Host-buffer path (reference contract): NumPy in, fp64 NumPy out, via one
+    rsr_multiply_host call (H2D + multiply + D2H + sync)."""
+    import torch
+    raw = np.asarray(v_in)
+    integer_input = raw.dtype.kind in "iub"
+    v = as_vector(v_in)
+    if v.shape[0] != idx.rows:
+        raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
+    if compute is None:
+        compute = "int32" if integer_input and np.abs(v).max(initial=0) < 2 ** 31 else "float64"
+    if compute == "int32":
+        vh = _staging.get("v_i32", idx.rows, torch.int32, True)
+        vh.numpy()[:] = v.astype(np.int32) if not integer_input else raw.astype(np.int32)
+        vcode, dv = _native.I32, _staging.get("dv_i32", idx.rows, torch.int32, False)
+    elif compute == "float64":
+        vh = _staging.get("v_f64", idx.rows, torch.float64, True)
+        vh.numpy()[:] = v
+        vcode, dv = _native.F64, _staging.get("dv_f64", idx.rows, torch.float64, False)
+    else:
+        raise ValueError("compute must be int32 or float64 for host vectors")
+    oh = _staging.get("o_f64", idx.cols, torch.float64, True)
+    do = _staging.get("do_f64", idx.cols, torch.float64, False)
+    _native.check(_native.lib().rsr_multiply_host(
+        ctypes.byref(idx.desc), vh.data_ptr(), vcode, oh.data_ptr(), _native.F64,
+        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, dv.data_ptr(), do.data_ptr(),
+        _native.current_stream_ptr()))
+    return oh.numpy().copy()
+
+
+def _is_device_tensor(v) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(v, torch.Tensor) and v.is_cuda
+
+
+def multiply_rsr(v, idx: RsrIndex, variant: str = "rsrpp", *, compute: str | None = None):
+    """v times the indexed binary matrix; block results concatenated in order (kernels.py:185-193)."""
+    use_fold = _use_fold(variant)
+    if _is_device_tensor(v):
+        return _multiply_device(v, idx, use_fold)
+    return _multiply_host(v, idx, use_fold, compute)
+
+
+def multiply_ternary(v, idx: TernaryIndex, variant: str = "rsrpp", *, compute: str | None = None):
+    """v times the indexed ternary matrix: positive-half product minus negative-half
+    (kernels.py:196-206), fused into one launch."""
+    use_fold = _use_fold(variant)
+    if _is_device_tensor(v):
+        return _multiply_device(v, idx, use_fold)
+    return _multiply_host(v, idx, use_fold, compute)
+
+
+def multiply_parallel(v, idx, variant: str = "rsrpp", worker_count: int = 1, *, compute: str | None = None):
+    """Blocks partitioned across workers, each writing a disjoint output slice
+    (kernels.py:209-239).  Each worker's block range [i*nb//W, (i+1)*nb//W) is one
+    block-range launch on the current stream (the same partition the multi-GPU
+    path shards across ranks); the result is bitwise independent of W."""
+    import torch
+    use_fold = _use_fold(variant)
+    if worker_count < 1:
+        raise ValueError("worker_count must be at least 1")
+    device_in = _is_device_tensor(v)
+    if device_in:
+        dv = v
+    else:
+        vv = as_vector(v)
+        if vv.shape[0] != idx.rows:
+            raise ValueError(f"vector length {vv.shape[0]} does not match {idx.rows} rows")
+        raw = np.asarray(v)
+        if compute == "int32" or (compute is None and raw.dtype.kind in "iub"):
+            dv = torch.from_numpy(vv.astype(np.int32)).cuda()
+        else:
+            dv = torch.from_numpy(vv).cuda()
+    if dv.shape[0] != idx.rows:
+        raise ValueError(f"vector length {dv.shape[0]} does not match {idx.rows} rows")
+    out_dtype = torch.float64 if (not device_in) else dv.dtype
+    out = torch.empty(idx.cols, dtype=out_dtype, device=dv.device)
+    nb = idx.desc.nblocks
+    bounds = [i * nb // worker_count for i in range(worker_count + 1)]
+    for lo, hi in zip(bounds, bounds[1:]):
+        if lo < hi:
+            _multiply_device(dv, idx, use_fold, (lo, hi), out)
+    return out if device_in else out.cpu().numpy()
+
+
+def multiply_batched(V, idx, variant: str = "rsrpp"):
+    """V [batch, rows] CUDA tensor -> [batch, cols] (one multiply per row of V)."""
+    import torch
+    use_fold = _use_fold(variant)
+    if not _is_device_tensor(V) or V.dim() != 2 or V.shape[1] != idx.rows:
+        raise ValueError("V must be a CUDA tensor of shape [batch, rows]")
+    V = V.contiguous()
+    out = torch.empty((V.shape[0], idx.cols), dtype=V.dtype, device=V.device)
+    code = _torch_dtype_code(V)
+    _native.check(_native.lib().rsr_multiply_batched(
+        ctypes.byref(idx.desc), V.data_ptr(), code, V.shape[0], out.data_ptr(), code,
+        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, _native.current_stream_ptr()))
+    return out

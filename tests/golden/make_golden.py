@@ -1,0 +1,146 @@
+"""Generate golden vectors by running the REAL reference `rsr` package.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  The GPU box never reads /root/reference; tests
+only read these committed fixtures.  Every fixture records the reference call
+that produced it.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.environ.get("RSR_REFERENCE_SRC", "/root/reference/pkg/src"))
+import rsr  # noqa: E402  (the reference package)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def pack_index(prefix: str, idx, store: dict) -> None:
+    """Flatten one reference RsrIndex (indexer.py:47-139) into npz arrays."""
+    store[prefix + "perms"] = np.stack([blk.permutation for blk in idx.blocks]).astype(np.uint32)
+    store[prefix + "segs"] = np.asarray(idx._segs, np.int64)        # flat, each block 2^w + 1
+    store[prefix + "seg_starts"] = np.asarray(idx._seg_starts, np.int64)
+    store[prefix + "widths"] = np.asarray(idx._widths, np.int64)
+    store[prefix + "buckets"] = np.asarray(idx._buckets).astype(np.uint32)
+
+
+def worked_example() -> dict:
+    """conftest.py:10-26 / test_acceptance.py:88-101 known answers."""
+    B6 = np.array([[0, 1, 1, 1, 0, 1], [0, 0, 0, 1, 1, 1], [0, 1, 1, 1, 1, 0],
+                   [1, 1, 0, 0, 1, 0], [0, 0, 1, 1, 0, 1], [0, 0, 0, 0, 1, 0]], np.uint8)
+    V6 = np.array([3.0, 2.0, 4.0, 5.0, 9.0, 1.0])
+    B = rsr.BinaryMatrix.from_dense(B6)
+    idx = rsr.preprocess(B, 2)
+    tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(B6.astype(np.int8)), 2)
+    u = rsr.segmented_sum(V6, idx.blocks[0])
+    out = {"B6": B6, "V6": V6,
+           "block0_perm": idx.blocks[0].permutation, "block0_seg": idx.blocks[0].segmentation,
+           "block0_sums": u.sums, "block0_rsr": rsr.block_product_rsr(u),
+           "block0_rsrpp": rsr.block_product_rsrpp(u),
+           "product_binary": rsr.multiply_rsr(V6, idx), "product_ternary": rsr.multiply_ternary(V6, tidx),
+           "naive": rsr.naive_multiply(V6, B)}
+    pack_index("bidx_", idx, out)
+    pack_index("tpos_", tidx.positive, out)
+    pack_index("tneg_", tidx.negative, out)
+    return out
+
+
+def fuzz_cases(seed: int, count: int, max_dim: int, ks_cap: int) -> dict:
+    """Seeded small ternary cases across k (criterion-1 style, test_acceptance.py:41-64):
+    matrix, integer and float vectors, full reference index, rsr/rsrpp products."""
+    rng = np.random.default_rng(seed)
+    out = {"count": np.int64(count)}
+    for i in range(count):
+        rows = int(rng.integers(1, max_dim + 1))
+        cols = int(rng.integers(1, max_dim + 1))
+        A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        vi = rng.integers(-100, 101, size=rows).astype(np.float64)
+        vf = rng.standard_normal(rows)
+        kmax = min(ks_cap, rsr.max_k_for_rows(rows))
+        k = int(rng.integers(1, kmax + 1))
+        T = rsr.TernaryMatrix(A)
+        tidx = rsr.preprocess_ternary(T, k)
+        p = f"c{i}_"
+        out[p + "A"] = A
+        out[p + "k"] = np.int64(k)
+        out[p + "vi"] = vi
+        out[p + "vf"] = vf
+        pack_index(p + "pos_", tidx.positive, out)
+        pack_index(p + "neg_", tidx.negative, out)
+        for variant in ("rsr", "rsrpp"):
+            out[p + f"int_{variant}"] = rsr.multiply_ternary(vi, tidx, variant)
+            out[p + f"flt_{variant}"] = rsr.multiply_ternary(vf, tidx, variant)
+        out[p + "int_naive"] = rsr.naive_multiply(vi, T)
+        out[p + "flt_naive"] = rsr.naive_multiply(vf, T)
+        # binary multiply of the positive half (multiply_rsr, kernels.py:185-193)
+        out[p + "int_pos_rsrpp"] = rsr.multiply_rsr(vi, tidx.positive, "rsrpp")
+    return out
+
+
+def medium_cases() -> dict:
+    """The criterion-1 'big' shapes (test_acceptance.py:46-48) at tuned k, integer v:
+    products only plus the seeded generator, so tests can regenerate the inputs."""
+    out = {}
+    for i, (rows, cols) in enumerate(((256, 256), (1024, 1024), (256, 1024), (1024, 256))):
+        rng = np.random.default_rng([2411, rows, cols])
+        A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        v = rng.integers(-100, 101, size=rows).astype(np.float64)
+        k = rsr.optimal_k_rsrpp(rows)
+        tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+        p = f"m{i}_"
+        out[p + "shape"] = np.array([rows, cols], np.int64)
+        out[p + "k"] = np.int64(k)
+        out[p + "rsrpp"] = rsr.multiply_ternary(v, tidx, "rsrpp")
+        out[p + "rsr"] = rsr.multiply_ternary(v, tidx, "rsr")
+        out[p + "naive"] = rsr.naive_multiply(v, rsr.TernaryMatrix(A))
+        out[p + "pos_perm_crc"] = np.array([int(np.bitwise_xor.reduce(
+            blk.permutation.astype(np.uint64) * np.arange(1, rows + 1, dtype=np.uint64)))
+            for blk in tidx.positive.blocks], np.uint64)
+        out[p + "neg_seg_sum"] = np.array([int(blk.segmentation.astype(np.int64).sum())
+                                           for blk in tidx.negative.blocks], np.int64)
+    return out
+
+
+def folds() -> dict:
+    """Block products (kernels.py:104-116) on integer and float u, widths 1..10."""
+    rng = np.random.default_rng(104)
+    out = {}
+    for w in range(1, 11):
+        ui = rng.integers(-100, 101, size=1 << w).astype(np.float64)
+        uf = rng.standard_normal(1 << w)
+        for tag, u in (("i", ui), ("f", uf)):
+            s = rsr.SegmentedSums(w, u)
+            out[f"w{w}{tag}_u"] = u
+            out[f"w{w}{tag}_rsr"] = rsr.block_product_rsr(s)
+            out[f"w{w}{tag}_rsrpp"] = rsr.block_product_rsrpp(s)
+    return out
+
+
+def tuner() -> dict:
+    ns = np.array(sorted(set([1, 2, 3, 6, 100, 4095, 4096, 14336, 16384, 65536]
+                             + [1 << e for e in range(0, 17)]
+                             + list(np.random.default_rng(8).integers(1, 1 << 17, 200)))), np.int64)
+    return {"n": ns,
+            "k_rsrpp": np.array([rsr.optimal_k_rsrpp(int(n)) for n in ns], np.int64),
+            "k_rsr": np.array([rsr.optimal_k_rsr(int(n)) for n in ns], np.int64),
+            "max_k": np.array([rsr.max_k_for_rows(int(n)) for n in ns], np.int64)}
+
+
+def main() -> None:
+    np.savez_compressed(os.path.join(HERE, "worked_example.npz"), **worked_example())
+    np.savez_compressed(os.path.join(HERE, "fuzz_small.npz"), **fuzz_cases(101, 60, 64, 8))
+    np.savez_compressed(os.path.join(HERE, "medium.npz"), **medium_cases())
+    np.savez_compressed(os.path.join(HERE, "folds.npz"), **folds())
+    np.savez_compressed(os.path.join(HERE, "tuner.npz"), **tuner())
+    print("reference rsr", rsr.__version__, "golden vectors written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,258 @@
+"""Parity of the sm_100a CUDA path against the oracle and the reference's golden vectors.
+
+Bars: bit-exact for indices (perm / seg / keys) and for integer activations with
+int32 accumulation; fp64 activations within the reference's own float test
+tolerance (rtol = atol = 1e-9, test_kernels.py:269-280); fp32 activations within
+||got - ref||_inf <= 1e-5 * max(||ref||_inf, 1) (north star, norm-wise).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import unpack_index
+from oracle import c_oracle
+from oracle import rsr_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+
+
+def _fp32_ok(got, ref):
+    got = np.asarray(got, np.float64)
+    scale = max(float(np.abs(ref).max(initial=0.0)), 1.0)
+    return float(np.abs(got - ref).max(initial=0.0)) <= FP32_TOL * scale
+
+
+def _dev_index_arrays(idx):
+    perm, seg, bucket = idx.host_arrays()
+    return perm, seg, bucket
+
+
+# ----------------------------------------------------------------------------- worked example
+def test_worked_example(rsr, cuda, worked):
+    B = rsr.BinaryMatrix.from_dense(worked["B6"])
+    idx = rsr.preprocess(B, 2)
+    assert idx.block_count == 3 and (idx.rows, idx.cols, idx.k) == (6, 6, 2)
+    assert np.array_equal(idx.blocks[0].permutation, [1, 4, 5, 0, 2, 3])
+    assert np.array_equal(idx.blocks[0].segmentation, [0, 3, 5, 5])
+    u = rsr.segmented_sum(worked["V6"], idx.blocks[0])
+    assert np.array_equal(u.sums, [12.0, 7.0, 0.0, 5.0])
+    assert np.array_equal(rsr.block_product_rsr(u), [5.0, 12.0])
+    assert np.array_equal(rsr.block_product_rsrpp(u), [5.0, 12.0])
+    tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(worked["B6"].astype(np.int8)), 2)
+    for variant in ("rsr", "rsrpp", "rsr++"):
+        assert np.array_equal(rsr.multiply_rsr(worked["V6"], idx, variant), worked["product_binary"])
+        assert np.array_equal(rsr.multiply_ternary(worked["V6"], tidx, variant), worked["product_ternary"])
+    for blk in tidx.negative.blocks:
+        assert np.array_equal(blk.segmentation, [0, 6, 6, 6])
+    assert np.array_equal(rsr.naive_multiply(worked["V6"], B), worked["naive"])
+    assert rsr.reconstruct_matrix(idx) == B
+
+
+# ----------------------------------------------------------------------------- golden fuzz
+def test_preprocess_bitwise_vs_reference_golden(rsr, cuda, fuzz):
+    for i in range(int(fuzz["count"])):
+        p = f"c{i}_"
+        A, k = fuzz[p + "A"], int(fuzz[p + "k"])
+        tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+        for half, pre in ((tidx.positive, "pos_"), (tidx.negative, "neg_")):
+            rp, rs, rb = unpack_index(fuzz, p + pre)
+            perm, seg, bucket = _dev_index_arrays(half)
+            assert np.array_equal(perm, rp), (i, pre)
+            assert np.array_equal(bucket, rb), (i, pre)
+            for b, s in enumerate(rs):
+                assert np.array_equal(seg[b, :len(s)], s), (i, pre, b)
+
+
+def test_multiply_vs_reference_golden(rsr, cuda, fuzz):
+    import torch
+    for i in range(int(fuzz["count"])):
+        p = f"c{i}_"
+        A, k = fuzz[p + "A"], int(fuzz[p + "k"])
+        tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+        vi, vf = fuzz[p + "vi"], fuzz[p + "vf"]
+        for variant in ("rsr", "rsrpp"):
+            ref_i, ref_f = fuzz[p + f"int_{variant}"], fuzz[p + f"flt_{variant}"]
+            # reference contract: NumPy fp64 in -> fp64 out (gather kernel in fp64)
+            assert np.array_equal(rsr.multiply_ternary(vi, tidx, variant), ref_i)
+            np.testing.assert_allclose(rsr.multiply_ternary(vf, tidx, variant), ref_f, rtol=1e-9, atol=1e-9)
+            # integer NumPy input -> int32 scatter kernel, fp64 result
+            assert np.array_equal(rsr.multiply_ternary(vi.astype(np.int64), tidx, variant), ref_i)
+            # device tensors
+            dvi = torch.from_numpy(vi.astype(np.int32)).cuda()
+            got = rsr.multiply_ternary(dvi, tidx, variant)
+            assert got.dtype == torch.int32 and np.array_equal(got.cpu().numpy(), ref_i)
+            dvf = torch.from_numpy(vf.astype(np.float32)).cuda()
+            ref32 = O.multiply_ternary(vf.astype(np.float32).astype(np.float64),
+                                       unpack_index(fuzz, p + "pos_")[2], unpack_index(fuzz, p + "neg_")[2],
+                                       A.shape[1], k, variant == "rsrpp")
+            assert _fp32_ok(rsr.multiply_ternary(dvf, tidx, variant).cpu().numpy(), ref32)
+            # deterministic int32 gather form agrees bitwise with the scatter form
+            from paper_2411_06360_b200 import kernels as K, _native
+            g = K._multiply_device(dvi, tidx, variant == "rsrpp", form=_native.FORM_GATHER)
+            assert np.array_equal(g.cpu().numpy(), ref_i)
+        assert np.array_equal(rsr.multiply_rsr(vi, tidx.positive, "rsrpp"), fuzz[p + "int_pos_rsrpp"])
+
+
+def test_medium_shapes_vs_reference(rsr, cuda, medium):
+    import torch
+    for i in range(4):
+        p = f"m{i}_"
+        rows, cols = (int(x) for x in medium[p + "shape"])
+        k = int(medium[p + "k"])
+        rng = np.random.default_rng([2411, rows, cols])
+        A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        v = rng.integers(-100, 101, size=rows).astype(np.float64)
+        tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+        for variant in ("rsrpp", "rsr"):
+            dv = torch.from_numpy(v.astype(np.int32)).cuda()
+            assert np.array_equal(rsr.multiply_ternary(dv, tidx, variant).cpu().numpy(), medium[p + variant])
+            assert np.array_equal(rsr.multiply_ternary(v, tidx, variant), medium[p + variant])
+        assert np.array_equal(rsr.naive_multiply(v, rsr.TernaryMatrix(A)), medium[p + "naive"])
+
+
+# ----------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("rows,cols,k", [
+    (1, 1, 1), (2, 1, 1), (3, 5, 1), (6, 6, 2), (9, 14, 3), (33, 65, 5), (64, 64, 6),
+    (100, 7, 6), (257, 300, 8), (1000, 129, 7), (4097, 50, 12), (300, 70, 1),
+])
+def test_edge_shapes_all_forms(rsr, cuda, rows, cols, k):
+    import torch
+    from paper_2411_06360_b200 import kernels as K, _native
+    rng = np.random.default_rng([rows, cols, k, 7])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    (pp, ps, pb), (np_, ns, nb) = c_oracle.preprocess_ternary(A, k)
+    tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+    perm, seg, bucket = _dev_index_arrays(tidx.positive)
+    assert np.array_equal(perm, pp) and np.array_equal(bucket, pb)
+    for b, s in enumerate(ps):
+        assert np.array_equal(seg[b, :len(s)], s)
+    vi = rng.integers(-100, 101, size=rows)
+    vf = rng.standard_normal(rows)
+    for fold in (True, False):
+        ref = c_oracle.multiply_parallel(vi.astype(np.float64), pb, nb, cols, k, fold, 1)
+        dv = torch.from_numpy(vi.astype(np.int32)).cuda()
+        for form in (_native.FORM_SCATTER, _native.FORM_GATHER):
+            got = K._multiply_device(dv, tidx, fold, form=form).cpu().numpy()
+            assert np.array_equal(got, ref), (form, fold)
+        reff = c_oracle.multiply_parallel(vf, pb, nb, cols, k, fold, 1)
+        np.testing.assert_allclose(rsr.multiply_ternary(vf, tidx, "rsrpp" if fold else "rsr"), reff,
+                                   rtol=1e-9, atol=1e-9)
+
+
+def test_zero_and_dense_extremes(rsr, cuda):
+    import torch
+    for A in (np.zeros((50, 23), np.int8), np.ones((50, 23), np.int8), -np.ones((50, 23), np.int8)):
+        tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), 4)
+        v = np.arange(50, dtype=np.int32) - 25
+        got = rsr.multiply_ternary(torch.from_numpy(v).cuda(), tidx).cpu().numpy()
+        assert np.array_equal(got, v.astype(np.int64) @ A.astype(np.int64))
+    tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(np.zeros((6, 3), np.int8)), 2)
+    assert np.array_equal(tidx.positive.blocks[0].permutation, np.arange(6))
+    assert np.array_equal(tidx.positive.blocks[0].segmentation, [0, 6, 6, 6])
+
+
+def test_row_splits_and_large_k(rsr, cuda):
+    """rows > 16384 exercises the multi-CTA row split (atomic output); k up to 15."""
+    import torch
+    for rows, cols, k in ((20000, 40, 11), (40000, 33, 15), (16385, 30, 13)):
+        rng = np.random.default_rng([rows, cols])
+        A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        v = rng.integers(-100, 101, size=rows).astype(np.int32)
+        (pp, ps, pb), (np_, ns, nb) = c_oracle.preprocess_ternary(A, k)
+        tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+        perm, seg, bucket = _dev_index_arrays(tidx.negative)
+        assert np.array_equal(perm, np_) and np.array_equal(bucket, nb)
+        ref = v.astype(np.int64) @ A.astype(np.int64)
+        for variant in ("rsrpp", "rsr"):
+            got = rsr.multiply_ternary(torch.from_numpy(v).cuda(), tidx, variant).cpu().numpy()
+            assert np.array_equal(got, ref), (rows, k, variant)
+            got = rsr.multiply_ternary(v.astype(np.float64), tidx, variant)
+            assert np.array_equal(got, ref)
+
+
+def test_device_k_limit_and_errors(rsr, cuda):
+    import torch
+    A = rsr.TernaryMatrix(np.ones((6, 6), np.int8))
+    with pytest.raises(ValueError):
+        rsr.preprocess_ternary(A, 3)
+    tidx = rsr.preprocess_ternary(A, 2)
+    with pytest.raises(ValueError, match="does not match"):
+        rsr.multiply_ternary(np.ones(5), tidx)
+    with pytest.raises(ValueError):
+        rsr.multiply_ternary(np.array([1.0, np.nan, 0, 0, 0, 0]), tidx)
+    with pytest.raises(ValueError, match="variant"):
+        rsr.multiply_ternary(np.ones(6), tidx, "fast")
+    with pytest.raises(ValueError, match="worker_count"):
+        rsr.multiply_parallel(np.ones(6), tidx, worker_count=0)
+    with pytest.raises(ValueError, match="does not match"):
+        rsr.multiply_ternary(torch.ones(5, dtype=torch.int32, device="cuda"), tidx)
+    bad = torch.tensor([[1, 2], [0, 1]], dtype=torch.int8, device="cuda")
+    with pytest.raises(ValueError, match="ternary entries"):
+        rsr.preprocess_ternary(bad, 1)
+
+
+def test_parallel_workers_bitwise_independent(rsr, cuda):
+    rng = np.random.default_rng(107)
+    n = 1 << 12
+    for case in range(6):
+        cols = int(rng.integers(512, 4097))
+        A = rng.integers(-1, 2, size=(n, cols), dtype=np.int8)
+        k = (8, 9, 10)[case % 3]
+        tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+        v = rng.integers(-100, 101, size=n) if case % 2 == 0 else rng.standard_normal(n)
+        for variant in ("rsr", "rsrpp"):
+            ref = rsr.multiply_ternary(v, tidx, variant)
+            for workers in (1, 2, 4, 8, 32):
+                got = rsr.multiply_parallel(v, tidx, variant, worker_count=workers)
+                assert got.tobytes() == ref.tobytes()
+
+
+def test_conservation_of_block_sums(rsr, cuda):
+    rng = np.random.default_rng(108)
+    for _ in range(10):
+        rows, cols = int(rng.integers(2, 129)), int(rng.integers(1, 129))
+        B = rsr.BinaryMatrix.from_dense(rng.integers(0, 2, size=(rows, cols), dtype=np.uint8))
+        v = rng.integers(-100, 101, size=rows).astype(np.float64)
+        for k in range(1, min(6, rsr.max_k_for_rows(rows)) + 1):
+            for blk in rsr.preprocess(B, k).blocks:
+                assert rsr.segmented_sum(v, blk).sums.sum() == v.sum()
+
+
+def test_binary_preprocess_and_row_order(rsr, cuda):
+    rng = np.random.default_rng(1)
+    dense = rng.integers(0, 2, size=(64, 20), dtype=np.uint8)
+    B = rsr.BinaryMatrix.from_dense(dense)
+    perms, segs, buckets = O.preprocess_binary(dense, 3)
+    idx = rsr.preprocess(B, 3)
+    perm, seg, bucket = idx.host_arrays()
+    assert np.array_equal(perm, perms) and np.array_equal(bucket, buckets)
+    assert np.array_equal(rsr.binary_row_order(B, (0, 3)), perms[0])
+    assert np.array_equal(rsr.full_segmentation(B, (0, 3), perms[0]), segs[0][:-1])
+    with pytest.raises(ValueError):
+        rsr.full_segmentation(B, (0, 3), np.arange(64))
+    for k in range(1, 7):
+        assert rsr.reconstruct_matrix(rsr.preprocess(B, k)) == B
+
+
+def test_from_blocks_round_trip_and_validation(rsr, cuda, worked):
+    B = rsr.BinaryMatrix.from_dense(worked["B6"])
+    idx = rsr.preprocess(B, 2)
+    blocks = [rsr.BlockIndex(b.width, b.permutation.copy(), b.segmentation.copy()) for b in idx.blocks]
+    rebuilt = rsr.RsrIndex.from_blocks(6, 6, 2, blocks)
+    assert rebuilt == idx
+    assert np.array_equal(rsr.multiply_rsr(worked["V6"], rebuilt), worked["product_binary"])
+    blocks[0].permutation[0] = blocks[0].permutation[1]
+    with pytest.raises(ValueError, match="bijection"):
+        rsr.RsrIndex.from_blocks(6, 6, 2, blocks)
+
+
+def test_block_products_bitwise(rsr, cuda, folds):
+    for w in range(1, 11):
+        for tag in ("i", "f"):
+            u = rsr.SegmentedSums(w, folds[f"w{w}{tag}_u"])
+            assert rsr.block_product_rsrpp(u).tobytes() == folds[f"w{w}{tag}_rsrpp"].tobytes()
+            assert rsr.block_product_rsr(u).tobytes() == folds[f"w{w}{tag}_rsr"].tobytes()
