@@ -238,7 +238,7 @@ def run_ours(args, cfg):
     kn = c_oracle.keys_ternary(A, k, -1) if domain == "ternary" else None
     halves = [idx.positive, idx.negative] if domain == "ternary" else [idx]
     for h, keys in zip(halves, [kp, kn]):
-        if not np.array_equal(h.device_tensors()["bucket"][:, :n].cpu().numpy(), keys):
+        if not np.array_equal(h.host_arrays()[2], keys):
             raise SystemExit("parity failure: device keys differ from the oracle")
     ref = c_oracle.multiply_parallel(v.astype(np.float64), kp, kn, m, k, True, cpu_threads())
     dv = torch.from_numpy(v).cuda()

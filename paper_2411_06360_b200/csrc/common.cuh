@@ -99,6 +99,14 @@ __device__ __forceinline__ T warp_inclusive_scan(T x, int lane) {
   return x;
 }
 
+// Device encoding of a bucket key (see multiply.cu): bank bits XOR-ed with the next five
+// bits.  An involution, so the same function encodes and decodes.
+__host__ __device__ __forceinline__ uint32_t key_swizzle(uint32_t j) { return j ^ ((j >> 5) & 31u); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __host__ __device__ __forceinline__ int block_width(int64_t cols, int k, int b) {
   int64_t rem = cols - (int64_t)b * k;
   return rem < k ? (int)rem : k;

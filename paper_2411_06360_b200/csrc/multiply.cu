@@ -28,6 +28,8 @@
 //    adds per bucket), or — for variant "rsr" — the segment sum u_j is formed
 //    and added to every column whose bit is set (w adds per bucket).  No
 //    floating-point atomics: results are deterministic run to run.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rsr {
@@ -39,105 +41,139 @@ constexpr int kMaxK = 16;
 constexpr int kRegFoldMaxK = 11;  // RSR++ register fold handles <= 2^11 bins; larger k folds top bits in smem
 
 // =====================================================================================
-// fold of one 2^K-bin int32 histogram by one warp -> r_s (s = LSB shift) in lane s.
-// Zeroes the histogram as it reads it.
+// Histogram layout.  Logical bin j lives at word key_swizzle(j) = j ^ ((j >> 5) & 31):
+// the low five bits (the shared-memory bank) are XOR-ed with the next five, which
+// flattens the skewed key distribution of a uniform ternary half (P[bit] = 1/3) from
+// 13% of atomics on bank 0 to ~5%.  The device bucket array stores keys already
+// swizzled, so the scatter loop adds no ALU work.  The swizzle only permutes bins
+// inside aligned 32-bin groups, and inside each int4 it is an XOR by (c & 3).
 // =====================================================================================
 
-__device__ __forceinline__ int32_t keep_if(int lane, int s, int32_t val) { return lane == s ? val : 0; }
-
-// RSR++: pairwise compaction (kernels.py:74-91).  Bits above kRegFoldMaxK are folded
-// first in shared memory from the top (r_top = sum of the upper half, u' = lower + upper),
-// the remaining <= 2^11 bins are folded in registers.
-__device__ int32_t fold_rsrpp_warp(int32_t* __restrict__ H, int K, int lane) {
-  int32_t mine = 0;
-  int Kc = K;
-  while (Kc > kRegFoldMaxK) {
-    const int half4 = 1 << (Kc - 3);  // int4 count of the lower half
-    int4* H4 = reinterpret_cast<int4*>(H);
-    int32_t acc = 0;
-    for (int q = lane; q < half4; q += 32) {
-      int4 a = H4[q], c = H4[q + half4];
-      acc += (c.x + c.y) + (c.z + c.w);
-      H4[q] = make_int4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
-      H4[q + half4] = make_int4(0, 0, 0, 0);
+// Recursive-halving warp reduce-scatter of 16 values: afterwards lanes 2i and 2i+1 hold
+// the warp total of a[i] (16 shuffles instead of 16 x 5).
+template <typename T>
+__device__ __forceinline__ T reduce_scatter16(T (&a)[16], int lane) {
+#pragma unroll
+  for (int step = 0; step < 4; ++step) {
+    const int half = 8 >> step;  // values kept after this step
+    const int bit = (lane >> (4 - step)) & 1;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const T keep = bit ? a[i + half] : a[i];
+      const T send = bit ? a[i] : a[i + half];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16 >> step);
     }
-    mine += keep_if(lane, Kc - 1, warp_sum(acc));
-    --Kc;
-    __syncwarp();
   }
-  if (Kc >= 7) {
-    // bins j = 4*(lane + 32*i) + e : bits 0-1 = e (local), bits 2-6 = lane, bits 7.. = i (local)
-    const int ni = 1 << (Kc - 7);
-    int4* H4 = reinterpret_cast<int4*>(H);
-    int32_t z[16];
-    int32_t p0 = 0, p1 = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (i < ni) {
-        int4 q = H4[lane + 32 * i];
-        H4[lane + 32 * i] = make_int4(0, 0, 0, 0);
-        p0 += q.y + q.w;
-        int32_t y0 = q.x + q.y, y1 = q.z + q.w;
-        p1 += y1;
-        z[i] = y0 + y1;
-      } else {
-        z[i] = 0;
-      }
-    }
-    mine += keep_if(lane, 0, warp_sum(p0));
-    mine += keep_if(lane, 1, warp_sum(p1));
-    // local i bits -> global bits 7..Kc-1
-#pragma unroll
-    for (int L = 0; L < 4; ++L) {
-      if (7 + L < Kc) {
-        const int cnt = ni >> (L + 1);
-        int32_t odd = 0;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          if (t < cnt) {
-            odd += z[2 * t + 1];
-            z[t] = z[2 * t] + z[2 * t + 1];
-          }
-        }
-        mine += keep_if(lane, 7 + L, warp_sum(odd));
-      }
-    }
-    const int32_t X = z[0];
-#pragma unroll
-    for (int s = 2; s < 7; ++s) mine += keep_if(lane, s, warp_sum(((lane >> (s - 2)) & 1) ? X : 0));
-  } else {
-    // scalar layout for <= 64 bins: bits 0-4 = lane, bit 5 = local
-    const int nb = 1 << Kc;
-    int32_t x0 = lane < nb ? H[lane] : 0;
-    int32_t x1 = (nb == 64) ? H[lane + 32] : 0;
-    if (lane < nb) H[lane] = 0;
-    if (nb == 64) H[lane + 32] = 0;
-    if (Kc == 6) mine += keep_if(lane, 5, warp_sum(x1));
-    const int32_t X = x0 + x1;
-    const int lb = Kc < 5 ? Kc : 5;
-    for (int s = 0; s < lb; ++s) mine += keep_if(lane, s, warp_sum(((lane >> s) & 1) ? X : 0));
-  }
-  return mine;
+  return a[0] + __shfl_xor_sync(0xffffffffu, a[0], 1);
 }
 
-// RSR: dense block product r_s = sum_j u[j] * bit_s(j) (kernels.py:63-71), K*2^K adds.
-__device__ int32_t fold_rsr_warp(int32_t* __restrict__ H, int K, int lane) {
-  int32_t acc[kMaxK];
+// Logical-order view of one int4 of swizzled bins: element e of the result is logical
+// bin 4q + e, given c = swizzle constant of the 32-bin group.
+__device__ __forceinline__ int4 unswizzle4(int4 q, uint32_t c) {
+  if (c & 1u) q = make_int4(q.y, q.x, q.w, q.z);
+  if (c & 2u) q = make_int4(q.z, q.w, q.x, q.y);
+  return q;
+}
+
+// One warp folds a 2^K-bin histogram (swizzled layout) into r_s, s = LSB shift, returned
+// in lanes 2s / 2s+1, and zeroes the histogram.  FOLDPP: RSR++ pairwise compaction
+// (kernels.py:74-91, 2*2^K adds); else the dense RSR product (kernels.py:63-71, K*2^K).
+template <bool FOLDPP>
+__device__ int32_t fold_warp(int32_t* __restrict__ H, int K, int lane) {
+  int32_t a[16];
 #pragma unroll
-  for (int s = 0; s < kMaxK; ++s) acc[s] = 0;
-  const int nb = 1 << K;
-  for (int j = lane; j < nb; j += 32) {
-    const int32_t u = H[j];
-    H[j] = 0;
+  for (int s = 0; s < 16; ++s) a[s] = 0;
+  int Kc = K;
+  if (FOLDPP) {
+    // bits above 2^11: fold from the top in shared memory (r_top = upper half; u' = lower + upper)
+    while (Kc > kRegFoldMaxK) {
+      const int half = 1 << (Kc - 1);
+      int32_t acc = 0;
+      for (int q = lane; q < half; q += 32) {
+        const uint32_t lo = key_swizzle((uint32_t)q), hi = key_swizzle((uint32_t)(q + half));
+        const int32_t x = H[hi];
+        acc += x;
+        H[lo] += x;
+        H[hi] = 0;
+      }
+      __syncwarp();
 #pragma unroll
-    for (int s = 0; s < kMaxK; ++s)
-      if (s < K) acc[s] += ((j >> s) & 1) ? u : 0;
+      for (int s = kRegFoldMaxK; s < 16; ++s)
+        if (s == Kc - 1) a[s] = acc;
+      --Kc;
+    }
   }
-  int32_t mine = 0;
+  if (Kc >= 7) {
+    // logical bins j = 4*(lane + 32*i) + e: bits 0-1 = e, 2-6 = lane, 7.. = i
+    const int ni = 1 << (Kc - 7);
+    int4* H4 = reinterpret_cast<int4*>(H);
+    int32_t X = 0;
+    if (FOLDPP) {
+      int32_t z[16];
 #pragma unroll
-  for (int s = 0; s < kMaxK; ++s)
-    if (s < K) mine += keep_if(lane, s, warp_sum(acc[s]));
-  return mine;
+      for (int i = 0; i < 16; ++i) {
+        z[i] = 0;
+        if (i < ni) {
+          const uint32_t c = (uint32_t)((lane >> 3) | (i << 2)) & 31u;  // (j >> 5) & 31
+          int4* slot = H4 + (((lane & 7) ^ (int)(c >> 2)) | (lane & ~7)) + 32 * i;
+          const int4 q = unswizzle4(*slot, c);
+          *slot = make_int4(0, 0, 0, 0);
+          a[0] += q.y + q.w;
+          const int32_t y1 = q.z + q.w;
+          a[1] += y1;
+          z[i] = q.x + q.y + y1;
+        }
+      }
+#pragma unroll
+      for (int L = 0; L < 4; ++L) {
+        if (7 + L < Kc) {
+          const int cnt = ni >> (L + 1);
+          int32_t odd = 0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if (t < cnt) {
+              odd += z[2 * t + 1];
+              z[t] = z[2 * t] + z[2 * t + 1];
+            }
+          }
+          a[7 + L] = odd;
+        }
+      }
+      X = z[0];
+    } else {
+      for (int i = 0; i < ni; ++i) {
+        const uint32_t c = (uint32_t)((lane >> 3) | (i << 2)) & 31u;
+        int4* slot = H4 + (((lane & 7) ^ (int)(c >> 2)) | (lane & ~7)) + 32 * i;
+        const int4 q = unswizzle4(*slot, c);
+        *slot = make_int4(0, 0, 0, 0);
+        const int32_t e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int ee = 0; ee < 4; ++ee) {
+          a[0] += (ee & 1) ? e[ee] : 0;
+          a[1] += (ee & 2) ? e[ee] : 0;
+#pragma unroll
+          for (int s = 7; s < 16; ++s)
+            if (s < Kc) a[s] += ((i >> (s - 7)) & 1) ? e[ee] : 0;
+          X += e[ee];
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 2; s < 7; ++s) a[s] = ((lane >> (s - 2)) & 1) ? X : 0;
+  } else {
+    // <= 64 bins: logical j = lane (+ 32); key_swizzle(j) = j for j < 32, j ^ 1 for 32..63
+    const int nb = 1 << Kc;
+    const int32_t x0 = lane < nb ? H[lane] : 0;
+    const int32_t x1 = (nb == 64) ? H[32 + (lane ^ 1)] : 0;
+    if (lane < nb) H[lane] = 0;
+    if (nb == 64) H[32 + lane] = 0;
+    a[5] = x1;
+    const int32_t X = x0 + x1;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) a[s] = ((lane >> s) & 1) ? X : 0;
+    if (Kc < 6) a[5] = 0;
+  }
+  return reduce_scatter16(a, lane);
 }
 
 // =====================================================================================
@@ -151,6 +187,8 @@ struct ScatterParams {
   int64_t rows, cols, row_stride;
   int k, halves, b_begin, b_end;
   int rows_per_cta, n_splits, stages, atomic_out, nhist;
+  int debug;  // diagnostic only (RSR_B200_DEBUG): 1 = skip atomics, 2 = skip fold
+  int v_aligned;
 };
 
 template <typename OutT>
@@ -159,18 +197,122 @@ __device__ __forceinline__ void emit(OutT* out, int64_t col, int32_t val, bool a
   else out[col] = (OutT)val;
 }
 
-template <int R, bool FOLDPP, typename OutT>
+constexpr int kPartialStride = 17;  // int32 slots per warp in the fold-partials table (odd: no bank conflicts)
+
+// Fold partial-vector slots (fixed, so no runtime register indexing):
+//   0..3  local-bit partials (bits [0, lb) of the key; lb <= 4)
+//   4..8  lane-bit partials  (key bits lb .. lb+4)
+//   9     warp total
+//   10..14 warp-bit partials (key bits lb+5 ..), formed in fold_combine
+__device__ __forceinline__ int slot_shift(int i, int lb) {
+  if (i < 4) return i < lb ? i : -1;
+  if (i < 9) return lb + (i - 4);
+  if (i >= 10 && i < 15) return lb + 5 + (i - 10);
+  return -1;
+}
+
+// Distributed fold, step 1 (every warp): the warp folds its own slice of the histogram.
+// Logical bin j = (warp*32 + lane) * 2^lb + e.  Local bits: RSR++ pairwise compaction
+// in registers (kernels.py:74-91) or, for "rsr", the dense product (kernels.py:63-71).
+template <bool FOLDPP>
+__device__ __forceinline__ void fold_slice(int32_t* __restrict__ H, int K, int lb, int warp, int lane,
+                                           int32_t* __restrict__ part) {
+  const int bpl = 1 << lb;
+  const int base = (warp * 32 + lane) * bpl;
+  int32_t a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = 0;
+  int32_t X = 0;
+  if (base < (1 << K)) {
+    int32_t x[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      x[e] = 0;
+      if (e < bpl) {
+        const uint32_t ph = key_swizzle((uint32_t)(base + e));
+        x[e] = H[ph];
+        H[ph] = 0;
+      }
+    }
+    if (FOLDPP) {
+#pragma unroll
+      for (int L = 0; L < 4; ++L) {
+        if (L < lb) {
+          const int cnt = bpl >> (L + 1);
+          int32_t odd = 0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if (t < cnt) {
+              odd += x[2 * t + 1];
+              x[t] = x[2 * t] + x[2 * t + 1];
+            }
+          }
+          a[L] = odd;
+        }
+      }
+      X = x[0];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        if (e < bpl) {
+#pragma unroll
+          for (int L = 0; L < 4; ++L) a[L] += ((e >> L) & 1) ? x[e] : 0;
+          X += x[e];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int bit = 0; bit < 5; ++bit) a[4 + bit] = ((lane >> bit) & 1) ? X : 0;
+  a[9] = X;
+  const int32_t r = reduce_scatter16(a, lane);  // lanes 2i, 2i+1 hold slot i
+  if (!(lane & 1) && (lane >> 1) < 10) part[warp * kPartialStride + (lane >> 1)] = r;
+}
+
+// Step 2 (the last warp to finish step 1): sum the per-warp partials; warp totals feed the
+// warp-index bits.  Returns slot totals in lanes 2i / 2i+1 (see slot_shift).
+__device__ __forceinline__ int32_t fold_combine(const int32_t* __restrict__ part, int nwarps, int lane) {
+  int32_t a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = 0;
+  if (lane < nwarps) {
+    const int32_t* pw = part + lane * kPartialStride;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) a[i] = pw[i];
+    const int32_t W = pw[9];
+#pragma unroll
+    for (int bit = 0; bit < 5; ++bit) a[10 + bit] = ((lane >> bit) & 1) ? W : 0;
+  }
+  return reduce_scatter16(a, lane);
+}
+
+// Persistent CTA (one per SM), every warp scatters; no __syncthreads in the steady state.
+//  * Ring slot s (1-D TMA, mbarrier full[s]) is refilled by the LAST warp to finish reading it.
+//  * Unit u scatters into histogram buffer u % NH.  After scattering unit u every warp folds
+//    its slice of unit u-1's histogram (waiting on hfull, rarely blocking), zeroes it and
+//    arrives on hfree; the last warp to store its slice partials combines them and writes
+//    the block's outputs.  Unit u waits on hfree only before reusing buffer u % NH.
+template <int R, bool FOLDPP, bool TERNARY, typename OutT>
 __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const ScatterParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int HALVES = TERNARY ? 2 : 1;
   const int T = blockDim.x;
+  const int nwarps = T >> 5;
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const int nbk = 1 << p.k;
   const int rpc = p.rows_per_cta;
   const int S = p.stages;
+  const int NH = p.nhist;
   int32_t* hist = reinterpret_cast<int32_t*>(smem);
-  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + sizeof(int32_t) * p.nhist * nbk);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)S * p.halves * rpc);
+  int32_t* parts = hist + NH * nbk;  // [NH][nwarps][kPartialStride]
+  uint16_t* ring = reinterpret_cast<uint16_t*>(
+      smem + ((sizeof(int32_t) * (NH * nbk + NH * nwarps * kPartialStride) + 127) & ~(size_t)127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * HALVES * rpc);
+  uint64_t* hfull = full + S;
+  uint64_t* hfree = hfull + NH;
+  int* slot_cnt = reinterpret_cast<int*>(hfree + NH);
+  int* comb_cnt = slot_cnt + S;
 
   const int split = blockIdx.x % p.n_splits;
   const int col_cta = blockIdx.x / p.n_splits;
@@ -183,74 +325,130 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
   const int rows_valid = (int)std::min<int64_t>(rpc, p.rows - r0);
   const uint16_t* key0 = p.key[0];
   const uint16_t* key1 = p.key[1];
+  // fold geometry: 2^lb bins per lane (nwarps is a power of two)
+  int lb = p.k - 5 - (31 - __clz(nwarps));
+  if (lb < 0) lb = 0;
 
-  // zero both histograms and the never-copied tail of every ring slot
-  for (int i = t; i < p.nhist * nbk; i += T) hist[i] = 0;
-  for (int sl = 0; sl < S * p.halves; ++sl)
+  for (int i = t; i < NH * nbk; i += T) hist[i] = 0;
+  for (int sl = 0; sl < S * HALVES; ++sl)
     for (int i = rows_copy + t; i < rpc; i += T) ring[(size_t)sl * rpc + i] = 0;
+  if (t < S) slot_cnt[t] = 0;
+  if (t < NH) comb_cnt[t] = 0;
 
-  // this CTA's slice of v lives in registers for the whole launch
+  uint64_t policy = 0;
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    for (int h = 0; h < NH; ++h) {
+      mbar_init(&hfull[h], nwarps);
+      mbar_init(&hfree[h], nwarps);
+    }
+    fence_mbar_init();
+    // start streaming the first S units before anything else
+    policy = l2_evict_first_policy();
+    for (int u = 0; u < S && u < nunits; ++u) {
+      const int b = p.b_begin + col_cta + u * ncol;
+      mbar_arrive_expect_tx(&full[u], copy_bytes * HALVES);
+      for (int h = 0; h < HALVES; ++h)
+        tma_load_1d(ring + ((size_t)u * HALVES + h) * rpc, (h ? key1 : key0) + (int64_t)b * p.row_stride + r0,
+                    copy_bytes, &full[u], policy);
+    }
+  }
+  // this CTA's slice of v lives in registers for the whole launch (16-byte loads)
   int32_t vr[R];
 #pragma unroll
   for (int g = 0; g < R / 8; ++g) {
     const int lr = 8 * (t + T * g);
+    if (lr + 8 <= rows_valid && p.v_aligned) {
+      const int4 a = *reinterpret_cast<const int4*>(p.v + r0 + lr);
+      const int4 c = *reinterpret_cast<const int4*>(p.v + r0 + lr + 4);
+      vr[g * 8 + 0] = a.x; vr[g * 8 + 1] = a.y; vr[g * 8 + 2] = a.z; vr[g * 8 + 3] = a.w;
+      vr[g * 8 + 4] = c.x; vr[g * 8 + 5] = c.y; vr[g * 8 + 6] = c.z; vr[g * 8 + 7] = c.w;
+    } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) vr[g * 8 + e] = (lr + e < rows_valid) ? p.v[r0 + lr + e] : 0;
-  }
-
-  if (t == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  uint64_t policy = 0;
-  if (t == 0) {
-    policy = l2_evict_first_policy();
-    for (int u = 0; u < S && u < nunits; ++u) {
-      const int b = p.b_begin + col_cta + u * ncol;
-      mbar_arrive_expect_tx(&bars[u], copy_bytes * p.halves);
-      for (int h = 0; h < p.halves; ++h)
-        tma_load_1d(ring + ((size_t)u * p.halves + h) * rpc, (h ? key1 : key0) + (int64_t)b * p.row_stride + r0, copy_bytes,
-                    &bars[u], policy);
+      for (int e = 0; e < 8; ++e) vr[g * 8 + e] = (lr + e < rows_valid) ? p.v[r0 + lr + e] : 0;
     }
   }
+  __syncthreads();
 
   OutT* out = reinterpret_cast<OutT*>(p.out);
-  for (int u = 0; u < nunits; ++u) {
-    const int stage = u % S;
-    const int b = p.b_begin + col_cta + u * ncol;
-    int32_t* H = hist + (p.nhist == 2 ? (u & 1) * nbk : 0);
-    mbar_wait(&bars[stage], (uint32_t)((u / S) & 1));
-    for (int h = 0; h < p.halves; ++h) {
-      const uint4* kk = reinterpret_cast<const uint4*>(ring + ((size_t)stage * p.halves + h) * rpc);
+  for (int u = 0; u <= nunits; ++u) {
+    if (u < nunits) {
+      const int stage = u % S;
+      const int hb = u % NH;
+      int32_t* H = hist + hb * nbk;
+      mbar_wait(&full[stage], (uint32_t)((u / S) & 1));
+      if (u >= NH) mbar_wait(&hfree[hb], (uint32_t)(((u / NH) - 1) & 1));
+      if (!(p.debug & 1)) {
+        uint4 q[HALVES][R / 8];
 #pragma unroll
-      for (int g = 0; g < R / 8; ++g) {
-        if (8 * (t + T * g) < rows_valid) {
-          const uint4 q = kk[t + T * g];
-          const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+        for (int h = 0; h < HALVES; ++h) {
+          const uint4* kk = reinterpret_cast<const uint4*>(ring + ((size_t)stage * HALVES + h) * rpc);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
-            atomicAdd(&H[w4[e] & 0xffffu], h ? -a : a);
-            atomicAdd(&H[w4[e] >> 16], h ? -c : c);
+          for (int g = 0; g < R / 8; ++g) q[h][g] = kk[t + T * g];
+        }
+#pragma unroll
+        for (int h = 0; h < HALVES; ++h) {
+#pragma unroll
+          for (int g = 0; g < R / 8; ++g) {
+            if (8 * (t + T * g) < rows_valid) {
+              const uint32_t w4[4] = {q[h][g].x, q[h][g].y, q[h][g].z, q[h][g].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
+                atomicAdd(&H[w4[e] & 0xffffu], h ? -a : a);
+                atomicAdd(&H[w4[e] >> 16], h ? -c : c);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        mbar_arrive(&hfull[hb]);
+        if (atomicAdd(&slot_cnt[stage], 1) == nwarps - 1) {  // every warp is done with this ring slot
+          slot_cnt[stage] = 0;
+          if (u + S < nunits) {
+            if (policy == 0) policy = l2_evict_first_policy();
+            fence_proxy_async_smem();
+            const int bn = p.b_begin + col_cta + (u + S) * ncol;
+            mbar_arrive_expect_tx(&full[stage], copy_bytes * HALVES);
+            for (int h = 0; h < HALVES; ++h)
+              tma_load_1d(ring + ((size_t)stage * HALVES + h) * rpc,
+                          (h ? key1 : key0) + (int64_t)bn * p.row_stride + r0, copy_bytes, &full[stage], policy);
           }
         }
       }
     }
-    __syncthreads();  // histogram complete, ring slot consumed
-    if (t == 0 && u + S < nunits) {
-      const int bn = p.b_begin + col_cta + (u + S) * ncol;
-      mbar_arrive_expect_tx(&bars[stage], copy_bytes * p.halves);
-      for (int h = 0; h < p.halves; ++h)
-        tma_load_1d(ring + ((size_t)stage * p.halves + h) * rpc, (h ? key1 : key0) + (int64_t)bn * p.row_stride + r0,
-                    copy_bytes, &bars[stage], policy);
+    if (u >= 1) {
+      // fold my slice of unit f = u-1
+      const int f = u - 1;
+      const int fb = f % NH;
+      int32_t* H = hist + fb * nbk;
+      int32_t* part = parts + fb * nwarps * kPartialStride;
+      mbar_wait(&hfull[fb], (uint32_t)((f / NH) & 1));
+      if (!(p.debug & 2)) fold_slice<FOLDPP>(H, p.k, lb, warp, lane, part);
+      else if (lane < nbk) H[lane] = 0;
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        mbar_arrive(&hfree[fb]);
+        if (atomicAdd(&comb_cnt[fb], 1) == nwarps - 1) {
+          comb_cnt[fb] = 0;
+          last = 1;
+        }
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence_block();
+        const int b = p.b_begin + col_cta + f * ncol;
+        const int32_t r = (p.debug & 2) ? 0 : fold_combine(part, nwarps, lane);
+        const int w = block_width(p.cols, p.k, b);
+        const int sh = slot_shift(lane >> 1, lb);
+        if (!(lane & 1) && sh >= 0 && sh < w) emit(out, (int64_t)b * p.k + (w - 1 - sh), r, p.atomic_out != 0);
+      }
     }
-    if (warp == (u & 31) % (T >> 5)) {
-      const int32_t r = FOLDPP ? fold_rsrpp_warp(H, p.k, lane) : fold_rsr_warp(H, p.k, lane);
-      const int w = block_width(p.cols, p.k, b);
-      if (lane < w) emit(out, (int64_t)b * p.k + (w - 1 - lane), r, p.atomic_out != 0);
-    }
-    if (p.nhist == 1) __syncthreads();  // single histogram: zeroed before the next scatter
   }
 }
 
@@ -476,7 +674,7 @@ __global__ void naive_ternary_kernel(const int8_t* __restrict__ A, int64_t rows,
 
 template <int R, bool PP, typename OutT>
 rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
-  auto kern = scatter_kernel<R, PP, OutT>;
+  auto kern = p.halves == 2 ? scatter_kernel<R, PP, true, OutT> : scatter_kernel<R, PP, false, OutT>;
   rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "scatter smem attribute");
   if (st != RSR_OK) return st;
@@ -492,10 +690,11 @@ rsr_status launch_scatter_r(const ScatterParams& p, bool pp, int grid, size_t sm
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out, rsr_dtype out_dtype, bool pp,
                             int b0, int b1, cudaStream_t s) {
-  if (d.k > 15) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply supports k <= 15");
+  if (d.k > 14) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply supports k <= 14");
   ScatterParams p{};
   for (int h = 0; h < d.halves; ++h) p.key[h] = d.half[h].bucket;
   p.v = v;
+  p.v_aligned = ((uintptr_t)v & 15) == 0;
   p.out = out;
   p.rows = d.rows;
   p.cols = d.cols;
@@ -506,25 +705,36 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
   p.b_end = b1;
   // rows per thread R (8 or 16), threads per CTA, row splits
   const int R = d.rows > 8192 ? 16 : 8;
-  int threads = kScatterThreads;
-  if (d.rows <= (int64_t)R * kScatterThreads) {
-    const int64_t need = (d.rows + R - 1) / R;
-    threads = (int)std::max<int64_t>(32, ((need + 31) / 32) * 32);
-  }
+  // power-of-two warp count: the distributed fold maps warp-index bits onto key bits
+  int threads = 32;
+  while (threads < kScatterThreads && (int64_t)threads * R < d.rows) threads *= 2;
   p.rows_per_cta = threads * R;
   p.n_splits = (int)((d.rows + p.rows_per_cta - 1) / p.rows_per_cta);
   p.atomic_out = p.n_splits > 1;
   const size_t slot_bytes = (size_t)d.halves * p.rows_per_cta * 2;
   const size_t max_smem = device_max_smem_optin();
-  // double-buffered histograms when they fit next to >= 2 ring stages, else one
-  p.nhist = (sizeof(int32_t) * 2 * ((size_t)1 << d.k) + 2 * slot_bytes + 256 <= max_smem) ? 2 : 1;
-  const size_t hist_bytes = sizeof(int32_t) * p.nhist * ((size_t)1 << d.k);
-  int stages = 4;
-  while (stages > 1 && hist_bytes + stages * slot_bytes + 8 * stages + 128 > max_smem) --stages;
-  if (hist_bytes + stages * slot_bytes + 8 * stages + 128 > max_smem)
-    return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: index slice does not fit in shared memory");
+  const size_t hist1 = sizeof(int32_t) * ((size_t)1 << d.k);
+  const int nwarps_cta = threads / 32;
+  auto need = [&](int st, int nh) {
+    return ((hist1 * nh + sizeof(int32_t) * nh * nwarps_cta * 17 + 127) & ~(size_t)127) + st * slot_bytes +
+           8 * (st + 2 * nh) + 4 * (st + nh) + 64;
+  };
+  {
+    const char* dbg = getenv("RSR_B200_DEBUG");
+    p.debug = dbg ? atoi(dbg) : 0;
+  }
+  // prefer >= 3 ring stages, then a second/third histogram buffer, then a 4th stage
+  int stages = 0, nhist = 0;
+  const int cand[][2] = {{3, 3}, {3, 2}, {4, 2}, {2, 2}, {1, 2}};  // the deferred fold needs >= 2 buffers
+  for (auto& c : cand)
+    if (need(c[0], c[1]) <= max_smem) { stages = c[0]; nhist = c[1]; break; }
+  if (!stages) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: index slice does not fit in shared memory");
+  if (stages == 3 && nhist == 3 && need(4, 3) <= max_smem) stages = 4;
+  if (const char* e = getenv("RSR_B200_STAGES")) stages = atoi(e);  // diagnostics
+  if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::max(2, atoi(e));
   p.stages = stages;
-  const size_t smem = hist_bytes + stages * slot_bytes + 8 * stages;
+  p.nhist = nhist;
+  const size_t smem = need(stages, nhist);
   const int nblk = b1 - b0;
   const int sms = device_sm_count();
   int ncol = std::max(1, std::min(nblk, sms / std::max(1, p.n_splits)));
@@ -587,7 +797,7 @@ rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* 
                     rsr_form form, int b0, int b1, cudaStream_t s) {
   const bool pp = var == RSR_VARIANT_RSRPP;
   if (b0 >= b1) return RSR_OK;
-  if (form == RSR_FORM_AUTO) form = vt == RSR_I32 ? RSR_FORM_SCATTER : RSR_FORM_GATHER;
+  if (form == RSR_FORM_AUTO) form = (vt == RSR_I32 && d.k <= 14) ? RSR_FORM_SCATTER : RSR_FORM_GATHER;
   if (form == RSR_FORM_SCATTER) {
     if (vt != RSR_I32) return fail(RSR_ERR_INVALID, "scatter form needs int32 activations");
     if (ot != RSR_I32 && ot != RSR_F64) return fail(RSR_ERR_INVALID, "int32 activations produce int32 or float64");
