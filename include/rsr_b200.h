@@ -56,8 +56,9 @@ typedef struct rsr_half_index {
   uint32_t* seg;    /* [nblocks][seg_stride]: seg[j] = #rows with key < j for
                        j < 2^w, seg[2^w] = rows (indexer.py:274-276 incl. sentinel) */
   uint16_t* bucket; /* [nblocks][row_stride]: key of every row, MSB-first
-                       (indexer.py:270 `_buckets`), stored bank-swizzled as
-                       key ^ ((key >> 5) & 31) (an involution); padding rows hold 0 */
+                       (indexer.py:270 `_buckets`), as a device code:
+                       swz(key) = key ^ ((key >> 5) & 31) (bank swizzle, an involution);
+                       padding rows hold 0 */
 } rsr_half_index;
 
 typedef struct rsr_index_desc {

@@ -103,6 +103,17 @@ __device__ __forceinline__ T warp_inclusive_scan(T x, int lane) {
 // bits.  An involution, so the same function encodes and decodes.
 __host__ __device__ __forceinline__ uint32_t key_swizzle(uint32_t j) { return j ^ ((j >> 5) & 31u); }
 
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+  return r;
+}
+
+// Shared-memory reduction (no return value): ATOMS.ADD on sm_100.
+__device__ __forceinline__ void red_add_shared(uint32_t addr, int32_t v) {
+  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

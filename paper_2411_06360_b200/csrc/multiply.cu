@@ -28,7 +28,9 @@
 //    adds per bucket), or — for variant "rsr" — the segment sum u_j is formed
 //    and added to every column whose bit is set (w adds per bucket).  No
 //    floating-point atomics: results are deterministic run to run.
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 
@@ -36,9 +38,9 @@ namespace rsr {
 
 namespace {
 
-constexpr int kScatterThreads = 1024;
+constexpr int kScatterThreads = 512;  // x kScatterR rows per thread = 16384 rows per CTA
+constexpr int kScatterR = 32;
 constexpr int kMaxK = 16;
-constexpr int kRegFoldMaxK = 11;  // RSR++ register fold handles <= 2^11 bins; larger k folds top bits in smem
 
 // =====================================================================================
 // Histogram layout.  Logical bin j lives at word key_swizzle(j) = j ^ ((j >> 5) & 31):
@@ -67,115 +69,6 @@ __device__ __forceinline__ T reduce_scatter16(T (&a)[16], int lane) {
   return a[0] + __shfl_xor_sync(0xffffffffu, a[0], 1);
 }
 
-// Logical-order view of one int4 of swizzled bins: element e of the result is logical
-// bin 4q + e, given c = swizzle constant of the 32-bin group.
-__device__ __forceinline__ int4 unswizzle4(int4 q, uint32_t c) {
-  if (c & 1u) q = make_int4(q.y, q.x, q.w, q.z);
-  if (c & 2u) q = make_int4(q.z, q.w, q.x, q.y);
-  return q;
-}
-
-// One warp folds a 2^K-bin histogram (swizzled layout) into r_s, s = LSB shift, returned
-// in lanes 2s / 2s+1, and zeroes the histogram.  FOLDPP: RSR++ pairwise compaction
-// (kernels.py:74-91, 2*2^K adds); else the dense RSR product (kernels.py:63-71, K*2^K).
-template <bool FOLDPP>
-__device__ int32_t fold_warp(int32_t* __restrict__ H, int K, int lane) {
-  int32_t a[16];
-#pragma unroll
-  for (int s = 0; s < 16; ++s) a[s] = 0;
-  int Kc = K;
-  if (FOLDPP) {
-    // bits above 2^11: fold from the top in shared memory (r_top = upper half; u' = lower + upper)
-    while (Kc > kRegFoldMaxK) {
-      const int half = 1 << (Kc - 1);
-      int32_t acc = 0;
-      for (int q = lane; q < half; q += 32) {
-        const uint32_t lo = key_swizzle((uint32_t)q), hi = key_swizzle((uint32_t)(q + half));
-        const int32_t x = H[hi];
-        acc += x;
-        H[lo] += x;
-        H[hi] = 0;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int s = kRegFoldMaxK; s < 16; ++s)
-        if (s == Kc - 1) a[s] = acc;
-      --Kc;
-    }
-  }
-  if (Kc >= 7) {
-    // logical bins j = 4*(lane + 32*i) + e: bits 0-1 = e, 2-6 = lane, 7.. = i
-    const int ni = 1 << (Kc - 7);
-    int4* H4 = reinterpret_cast<int4*>(H);
-    int32_t X = 0;
-    if (FOLDPP) {
-      int32_t z[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        z[i] = 0;
-        if (i < ni) {
-          const uint32_t c = (uint32_t)((lane >> 3) | (i << 2)) & 31u;  // (j >> 5) & 31
-          int4* slot = H4 + (((lane & 7) ^ (int)(c >> 2)) | (lane & ~7)) + 32 * i;
-          const int4 q = unswizzle4(*slot, c);
-          *slot = make_int4(0, 0, 0, 0);
-          a[0] += q.y + q.w;
-          const int32_t y1 = q.z + q.w;
-          a[1] += y1;
-          z[i] = q.x + q.y + y1;
-        }
-      }
-#pragma unroll
-      for (int L = 0; L < 4; ++L) {
-        if (7 + L < Kc) {
-          const int cnt = ni >> (L + 1);
-          int32_t odd = 0;
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            if (t < cnt) {
-              odd += z[2 * t + 1];
-              z[t] = z[2 * t] + z[2 * t + 1];
-            }
-          }
-          a[7 + L] = odd;
-        }
-      }
-      X = z[0];
-    } else {
-      for (int i = 0; i < ni; ++i) {
-        const uint32_t c = (uint32_t)((lane >> 3) | (i << 2)) & 31u;
-        int4* slot = H4 + (((lane & 7) ^ (int)(c >> 2)) | (lane & ~7)) + 32 * i;
-        const int4 q = unswizzle4(*slot, c);
-        *slot = make_int4(0, 0, 0, 0);
-        const int32_t e[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int ee = 0; ee < 4; ++ee) {
-          a[0] += (ee & 1) ? e[ee] : 0;
-          a[1] += (ee & 2) ? e[ee] : 0;
-#pragma unroll
-          for (int s = 7; s < 16; ++s)
-            if (s < Kc) a[s] += ((i >> (s - 7)) & 1) ? e[ee] : 0;
-          X += e[ee];
-        }
-      }
-    }
-#pragma unroll
-    for (int s = 2; s < 7; ++s) a[s] = ((lane >> (s - 2)) & 1) ? X : 0;
-  } else {
-    // <= 64 bins: logical j = lane (+ 32); key_swizzle(j) = j for j < 32, j ^ 1 for 32..63
-    const int nb = 1 << Kc;
-    const int32_t x0 = lane < nb ? H[lane] : 0;
-    const int32_t x1 = (nb == 64) ? H[32 + (lane ^ 1)] : 0;
-    if (lane < nb) H[lane] = 0;
-    if (nb == 64) H[32 + lane] = 0;
-    a[5] = x1;
-    const int32_t X = x0 + x1;
-#pragma unroll
-    for (int s = 0; s < 5; ++s) a[s] = ((lane >> s) & 1) ? X : 0;
-    if (Kc < 6) a[5] = 0;
-  }
-  return reduce_scatter16(a, lane);
-}
-
 // =====================================================================================
 // SCATTER kernel (int32)
 // =====================================================================================
@@ -187,7 +80,6 @@ struct ScatterParams {
   int64_t rows, cols, row_stride;
   int k, halves, b_begin, b_end;
   int rows_per_cta, n_splits, stages, atomic_out, nhist;
-  int debug;  // diagnostic only (RSR_B200_DEBUG): 1 = skip atomics, 2 = skip fold
   int v_aligned;
 };
 
@@ -197,257 +89,286 @@ __device__ __forceinline__ void emit(OutT* out, int64_t col, int32_t val, bool a
   else out[col] = (OutT)val;
 }
 
-constexpr int kPartialStride = 17;  // int32 slots per warp in the fold-partials table (odd: no bank conflicts)
-
-// Fold partial-vector slots (fixed, so no runtime register indexing):
-//   0..3  local-bit partials (bits [0, lb) of the key; lb <= 4)
-//   4..8  lane-bit partials  (key bits lb .. lb+4)
-//   9     warp total
-//   10..14 warp-bit partials (key bits lb+5 ..), formed in fold_combine
-__device__ __forceinline__ int slot_shift(int i, int lb) {
-  if (i < 4) return i < lb ? i : -1;
-  if (i < 9) return lb + (i - 4);
-  if (i >= 10 && i < 15) return lb + 5 + (i - 10);
-  return -1;
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
-// Distributed fold, step 1 (every warp): the warp folds its own slice of the histogram.
-// Logical bin j = (warp*32 + lane) * 2^lb + e.  Local bits: RSR++ pairwise compaction
-// in registers (kernels.py:74-91) or, for "rsr", the dense product (kernels.py:63-71).
-template <bool FOLDPP>
-__device__ __forceinline__ void fold_slice(int32_t* __restrict__ H, int K, int lb, int warp, int lane,
-                                           int32_t* __restrict__ part) {
-  const int bpl = 1 << lb;
-  const int base = (warp * 32 + lane) * bpl;
-  int32_t a[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a[i] = 0;
-  int32_t X = 0;
-  if (base < (1 << K)) {
-    int32_t x[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      x[e] = 0;
-      if (e < bpl) {
-        const uint32_t ph = key_swizzle((uint32_t)(base + e));
-        x[e] = H[ph];
-        H[ph] = 0;
-      }
-    }
-    if (FOLDPP) {
-#pragma unroll
-      for (int L = 0; L < 4; ++L) {
-        if (L < lb) {
-          const int cnt = bpl >> (L + 1);
-          int32_t odd = 0;
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            if (t < cnt) {
-              odd += x[2 * t + 1];
-              x[t] = x[2 * t] + x[2 * t + 1];
-            }
-          }
-          a[L] = odd;
-        }
-      }
-      X = x[0];
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        if (e < bpl) {
-#pragma unroll
-          for (int L = 0; L < 4; ++L) a[L] += ((e >> L) & 1) ? x[e] : 0;
-          X += x[e];
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int bit = 0; bit < 5; ++bit) a[4 + bit] = ((lane >> bit) & 1) ? X : 0;
-  a[9] = X;
-  const int32_t r = reduce_scatter16(a, lane);  // lanes 2i, 2i+1 hold slot i
-  if (!(lane & 1) && (lane >> 1) < 10) part[warp * kPartialStride + (lane >> 1)] = r;
+// Logical-order view of one int4 of swizzled bins: element e of the result is logical bin
+// 4q + e, given c = swizzle constant of the 32-bin group (key_swizzle XORs the low 5 bits).
+__device__ __forceinline__ int4 unswizzle4(int4 q, uint32_t c) {
+  if (c & 1u) q = make_int4(q.y, q.x, q.w, q.z);
+  if (c & 2u) q = make_int4(q.z, q.w, q.x, q.y);
+  return q;
 }
 
-// Step 2 (the last warp to finish step 1): sum the per-warp partials; warp totals feed the
-// warp-index bits.  Returns slot totals in lanes 2i / 2i+1 (see slot_shift).
-__device__ __forceinline__ int32_t fold_combine(const int32_t* __restrict__ part, int nwarps, int lane) {
-  int32_t a[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a[i] = 0;
-  if (lane < nwarps) {
-    const int32_t* pw = part + lane * kPartialStride;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) a[i] = pw[i];
-    const int32_t W = pw[9];
-#pragma unroll
-    for (int bit = 0; bit < 5; ++bit) a[10 + bit] = ((lane >> bit) & 1) ? W : 0;
-  }
-  return reduce_scatter16(a, lane);
-}
-
-// Persistent CTA (one per SM), every warp scatters; no __syncthreads in the steady state.
-//  * Ring slot s (1-D TMA, mbarrier full[s]) is refilled by the LAST warp to finish reading it.
-//  * Unit u scatters into histogram buffer u % NH.  After scattering unit u every warp folds
-//    its slice of unit u-1's histogram (waiting on hfull, rarely blocking), zeroes it and
-//    arrives on hfree; the last warp to store its slice partials combines them and writes
-//    the block's outputs.  Unit u waits on hfree only before reusing buffer u % NH.
+// Persistent CTA (up to 16 warps, one CTA per SM at n >= 8192), every warp scatters and folds.
+//  * Lane l of warp w owns rows w*32R + 256g + 8l + e (g < R/8, e < 8) of the CTA's row
+//    slice: their v values live in registers for the whole launch.  Each warp streams its
+//    rows' keys of every column block through a private S-slot shared-memory ring with 1-D
+//    TMA bulk copies (lane 0 issues, per-warp mbarriers) and refills a slot as soon as it
+//    has read it.  Key reads are conflict-free 16-byte loads (512 contiguous bytes per warp
+//    instruction) and are software-pipelined one half-unit ahead, so the shared-memory
+//    reductions of one half hide the load latency of the next.
+//  * Both halves of a ternary index scatter into ONE 2^k-bin histogram (+v for the positive
+//    key, -v for the negative key): the fold is linear, so fold(u+ - u-) is exactly the
+//    reference's `pos - neg` (kernels.py:206) in integer arithmetic.
+//  * Distributed fold: after scattering unit u, every warp folds its own 1/nwarps slice of
+//    unit u-1's histogram.  Bins j = (warp*32 + lane) * 2^lb + e: the e bits are folded in
+//    registers (RSR++ pairwise compaction, kernels.py:74-91, or the dense RSR product,
+//    kernels.py:63-71), lane bits by one warp reduce-scatter, warp bits are uniform; each
+//    warp then adds its share of the block's w outputs with one global reduction.
+//  * Histogram buffers are never zeroed: unit u adds into buffer u % NH on top of unit
+//    u - NH; each warp keeps its previous slice fold per buffer and adds only the
+//    difference (exact modulo 2^32).  Barriers: hfull[b] (all warps scattered) before the
+//    fold reads, hfree[b] (all warps read their slice) before the buffer is reused.
 template <int R, bool FOLDPP, bool TERNARY, typename OutT>
 __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const ScatterParams p) {
+  static_assert(R % 8 == 0 && R * kScatterThreads <= 16384, "rows per CTA");
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int HALVES = TERNARY ? 2 : 1;
+  constexpr int NG = R / 8;      // 8-row groups per lane
+  constexpr int WROWS = 32 * R;  // rows per warp
+  constexpr int MAXNH = 3;
   const int T = blockDim.x;
   const int nwarps = T >> 5;
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const int nbk = 1 << p.k;
-  const int rpc = p.rows_per_cta;
   const int S = p.stages;
   const int NH = p.nhist;
-  int32_t* hist = reinterpret_cast<int32_t*>(smem);
-  int32_t* parts = hist + NH * nbk;  // [NH][nwarps][kPartialStride]
-  uint16_t* ring = reinterpret_cast<uint16_t*>(
-      smem + ((sizeof(int32_t) * (NH * nbk + NH * nwarps * kPartialStride) + 127) & ~(size_t)127));
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * HALVES * rpc);
-  uint64_t* hfull = full + S;
+  const int hist_words = (NH * nbk + 15) & ~15;
+  int32_t* hist = reinterpret_cast<int32_t*>(smem);  // [NH][nbk]
+  uint16_t* ring_all = reinterpret_cast<uint16_t*>(smem + ((sizeof(int32_t) * hist_words + 127) & ~(size_t)127));
+  uint16_t* ring = ring_all + (size_t)warp * S * HALVES * WROWS;  // this warp's [S][HALVES][WROWS]
+  uint64_t* wfull_all = reinterpret_cast<uint64_t*>(ring_all + (size_t)nwarps * S * HALVES * WROWS);
+  uint64_t* wfull = wfull_all + warp * S;
+  uint64_t* hfull = wfull_all + nwarps * S;
   uint64_t* hfree = hfull + NH;
-  int* slot_cnt = reinterpret_cast<int*>(hfree + NH);
-  int* comb_cnt = slot_cnt + S;
 
   const int split = blockIdx.x % p.n_splits;
   const int col_cta = blockIdx.x / p.n_splits;
   const int ncol = gridDim.x / p.n_splits;
-  const int64_t r0 = (int64_t)split * rpc;
+  const int64_t r0 = (int64_t)split * p.rows_per_cta;
   const int nblk = p.b_end - p.b_begin;
   const int nunits = col_cta < nblk ? (nblk - col_cta + ncol - 1) / ncol : 0;
-  const int rows_copy = (int)std::min<int64_t>(rpc, p.row_stride - r0);  // multiple of 8
-  const uint32_t copy_bytes = (uint32_t)rows_copy * 2u;
-  const int rows_valid = (int)std::min<int64_t>(rpc, p.rows - r0);
+  const int64_t wr0 = r0 + (int64_t)warp * WROWS;  // first row of this warp
+  const int wcopy = (int)std::max<int64_t>(0, std::min<int64_t>(WROWS, p.row_stride - wr0));  // multiple of 8
+  const uint32_t wbytes = (uint32_t)wcopy * 2u;
+  // rows of my groups: wr0 + 256g + 8l + e; all valid iff the last group's 8 rows are < rows
+  const bool all_valid = wr0 + 256 * (NG - 1) + 8 * lane + 8 <= p.rows;
   const uint16_t* key0 = p.key[0];
   const uint16_t* key1 = p.key[1];
-  // fold geometry: 2^lb bins per lane (nwarps is a power of two)
-  int lb = p.k - 5 - (31 - __clz(nwarps));
+  const uint32_t hist_s = smem_u32(hist);
+  const uint32_t ring_s = smem_u32(ring);
+  OutT* out = reinterpret_cast<OutT*>(p.out);
+  // fold geometry: 2^lb bins per lane, warp index bits start at bit lb + 5
+  const int wbits = 31 - __clz(nwarps);
+  int lb = p.k - 5 - wbits;
   if (lb < 0) lb = 0;
+  const int fbase = (warp * 32 + lane) << lb;  // my first logical bin
+  const bool fold_active = fbase < nbk;
 
-  for (int i = t; i < NH * nbk; i += T) hist[i] = 0;
-  for (int sl = 0; sl < S * HALVES; ++sl)
-    for (int i = rows_copy + t; i < rpc; i += T) ring[(size_t)sl * rpc + i] = 0;
-  if (t < S) slot_cnt[t] = 0;
-  if (t < NH) comb_cnt[t] = 0;
-
-  uint64_t policy = 0;
-  if (t == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
-    for (int h = 0; h < NH; ++h) {
-      mbar_init(&hfull[h], nwarps);
-      mbar_init(&hfree[h], nwarps);
+  // 1. issue the loads of my rows of v (they stay in registers for the whole launch)
+  int32_t vr[R];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const int64_t row = wr0 + 256 * g + 8 * lane;
+    const int32_t* vp = p.v + row;
+    if (row + 8 <= p.rows && p.v_aligned) {
+      const int4 a = __ldg(reinterpret_cast<const int4*>(vp));
+      const int4 c = __ldg(reinterpret_cast<const int4*>(vp) + 1);
+      vr[8 * g + 0] = a.x; vr[8 * g + 1] = a.y; vr[8 * g + 2] = a.z; vr[8 * g + 3] = a.w;
+      vr[8 * g + 4] = c.x; vr[8 * g + 5] = c.y; vr[8 * g + 6] = c.z; vr[8 * g + 7] = c.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;
     }
+  }
+  // 2. start streaming this warp's keys of the first S units
+  uint64_t policy = 0;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&wfull[s], 1);
+    if (warp == 0)
+      for (int h = 0; h < NH; ++h) {
+        mbar_init(&hfull[h], nwarps);
+        mbar_init(&hfree[h], nwarps);
+      }
     fence_mbar_init();
-    // start streaming the first S units before anything else
     policy = l2_evict_first_policy();
     for (int u = 0; u < S && u < nunits; ++u) {
       const int b = p.b_begin + col_cta + u * ncol;
-      mbar_arrive_expect_tx(&full[u], copy_bytes * HALVES);
-      for (int h = 0; h < HALVES; ++h)
-        tma_load_1d(ring + ((size_t)u * HALVES + h) * rpc, (h ? key1 : key0) + (int64_t)b * p.row_stride + r0,
-                    copy_bytes, &full[u], policy);
+      mbar_arrive_expect_tx(&wfull[u], wbytes * HALVES);
+      if (wbytes)
+        for (int h = 0; h < HALVES; ++h)
+          tma_load_1d(ring + ((size_t)u * HALVES + h) * WROWS, (h ? key1 : key0) + (int64_t)b * p.row_stride + wr0,
+                      wbytes, &wfull[u], policy);
     }
   }
-  // this CTA's slice of v lives in registers for the whole launch (16-byte loads)
-  int32_t vr[R];
-#pragma unroll
-  for (int g = 0; g < R / 8; ++g) {
-    const int lr = 8 * (t + T * g);
-    if (lr + 8 <= rows_valid && p.v_aligned) {
-      const int4 a = *reinterpret_cast<const int4*>(p.v + r0 + lr);
-      const int4 c = *reinterpret_cast<const int4*>(p.v + r0 + lr + 4);
-      vr[g * 8 + 0] = a.x; vr[g * 8 + 1] = a.y; vr[g * 8 + 2] = a.z; vr[g * 8 + 3] = a.w;
-      vr[g * 8 + 4] = c.x; vr[g * 8 + 5] = c.y; vr[g * 8 + 6] = c.z; vr[g * 8 + 7] = c.w;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) vr[g * 8 + e] = (lr + e < rows_valid) ? p.v[r0 + lr + e] : 0;
+  // 3. zero the histograms; a single-split launch owns its output columns: zero them here
+  for (int i = t; i < hist_words / 4; i += T) reinterpret_cast<int4*>(hist)[i] = make_int4(0, 0, 0, 0);
+  if (!p.atomic_out)
+    for (int i = t; i < nunits * p.k; i += T) {
+      const int b = p.b_begin + col_cta + (i / p.k) * ncol;
+      const int c = i % p.k;
+      if (c < block_width(p.cols, p.k, b)) out[(int64_t)b * p.k + c] = (OutT)0;
     }
-  }
   __syncthreads();
 
-  OutT* out = reinterpret_cast<OutT*>(p.out);
+  int32_t prev[MAXNH];  // my previous slice fold of each buffer (lanes 2s: column shift s)
+#pragma unroll
+  for (int i = 0; i < MAXNH; ++i) prev[i] = 0;
+
+  // key loads of one half-unit: NG conflict-free 16-byte loads
+  auto load_keys = [&](int slot, int h, uint4 (&q)[NG]) {
+    const uint32_t base = ring_s + (uint32_t)(((slot * HALVES + h) * WROWS + 8 * lane) * 2);
+#pragma unroll
+    for (int g = 0; g < NG; ++g) q[g] = ld_shared_v4(base + (uint32_t)(g * 512));
+  };
+  uint4 q[NG];
+  if (nunits > 0) {
+    mbar_wait(&wfull[0], 0);
+    load_keys(0, 0, q);
+  }
+
   for (int u = 0; u <= nunits; ++u) {
     if (u < nunits) {
-      const int stage = u % S;
+      const int slot = u % S;
       const int hb = u % NH;
-      int32_t* H = hist + hb * nbk;
-      mbar_wait(&full[stage], (uint32_t)((u / S) & 1));
+      const uint32_t Hs = hist_s + (uint32_t)(hb * nbk) * 4u;
       if (u >= NH) mbar_wait(&hfree[hb], (uint32_t)(((u / NH) - 1) & 1));
-      if (!(p.debug & 1)) {
-        uint4 q[HALVES][R / 8];
 #pragma unroll
-        for (int h = 0; h < HALVES; ++h) {
-          const uint4* kk = reinterpret_cast<const uint4*>(ring + ((size_t)stage * HALVES + h) * rpc);
+      for (int h = 0; h < HALVES; ++h) {
+        // prefetch the next half-unit's keys before issuing this half's reductions
+        uint4 qn[NG];
+        if (h + 1 < HALVES) {
+          load_keys(slot, h + 1, qn);
+        } else if (u + 1 < nunits) {
+          const int ns = (u + 1) % S;
+          mbar_wait(&wfull[ns], (uint32_t)(((u + 1) / S) & 1));
+          load_keys(ns, 0, qn);
+        } else {
 #pragma unroll
-          for (int g = 0; g < R / 8; ++g) q[h][g] = kk[t + T * g];
+          for (int g = 0; g < NG; ++g) qn[g] = make_uint4(0, 0, 0, 0);
         }
+        if (all_valid) {
 #pragma unroll
-        for (int h = 0; h < HALVES; ++h) {
+          for (int g = 0; g < NG; ++g) {
+            const uint32_t w4[4] = {q[g].x, q[g].y, q[g].z, q[g].w};
 #pragma unroll
-          for (int g = 0; g < R / 8; ++g) {
-            if (8 * (t + T * g) < rows_valid) {
-              const uint32_t w4[4] = {q[h][g].x, q[h][g].y, q[h][g].z, q[h][g].w};
+            for (int e = 0; e < 4; ++e) {
+              const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
+              red_add_shared(Hs + ((w4[e] & 0xffffu) << 2), h ? -a : a);
+              red_add_shared(Hs + ((w4[e] >> 16) << 2), h ? -c : c);
+            }
+          }
+        } else {  // rows past the end of the matrix were never copied: skip them
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
-                atomicAdd(&H[w4[e] & 0xffffu], h ? -a : a);
-                atomicAdd(&H[w4[e] >> 16], h ? -c : c);
-              }
+          for (int g = 0; g < NG; ++g) {
+            const int64_t row = wr0 + 256 * g + 8 * lane;
+            const uint32_t w4[4] = {q[g].x, q[g].y, q[g].z, q[g].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
+              if (row + 2 * e < p.rows) red_add_shared(Hs + ((w4[e] & 0xffffu) << 2), h ? -a : a);
+              if (row + 2 * e + 1 < p.rows) red_add_shared(Hs + ((w4[e] >> 16) << 2), h ? -c : c);
             }
           }
         }
+#pragma unroll
+        for (int g = 0; g < NG; ++g) q[g] = qn[g];
       }
       __syncwarp();
       if (lane == 0) {
-        __threadfence_block();
-        mbar_arrive(&hfull[hb]);
-        if (atomicAdd(&slot_cnt[stage], 1) == nwarps - 1) {  // every warp is done with this ring slot
-          slot_cnt[stage] = 0;
-          if (u + S < nunits) {
-            if (policy == 0) policy = l2_evict_first_policy();
-            fence_proxy_async_smem();
-            const int bn = p.b_begin + col_cta + (u + S) * ncol;
-            mbar_arrive_expect_tx(&full[stage], copy_bytes * HALVES);
+        mbar_arrive(&hfull[hb]);  // release: this warp's reductions are visible to the folds
+        if (u + S < nunits) {     // refill my slot (all its keys are in registers already)
+          const int bn = p.b_begin + col_cta + (u + S) * ncol;
+          mbar_arrive_expect_tx(&wfull[slot], wbytes * HALVES);
+          if (wbytes)
             for (int h = 0; h < HALVES; ++h)
-              tma_load_1d(ring + ((size_t)stage * HALVES + h) * rpc,
-                          (h ? key1 : key0) + (int64_t)bn * p.row_stride + r0, copy_bytes, &full[stage], policy);
-          }
+              tma_load_1d(ring + ((size_t)slot * HALVES + h) * WROWS,
+                          (h ? key1 : key0) + (int64_t)bn * p.row_stride + wr0, wbytes, &wfull[slot], policy);
         }
       }
     }
-    if (u >= 1) {
-      // fold my slice of unit f = u-1
-      const int f = u - 1;
+    // fold my slice of unit f = u-1
+    const int f = u - 1;
+    if (f >= 0) {
       const int fb = f % NH;
-      int32_t* H = hist + fb * nbk;
-      int32_t* part = parts + fb * nwarps * kPartialStride;
+      const int32_t* H = hist + fb * nbk;
       mbar_wait(&hfull[fb], (uint32_t)((f / NH) & 1));
-      if (!(p.debug & 2)) fold_slice<FOLDPP>(H, p.k, lb, warp, lane, part);
-      else if (lane < nbk) H[lane] = 0;
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) {
-        __threadfence_block();
-        mbar_arrive(&hfree[fb]);
-        if (atomicAdd(&comb_cnt[fb], 1) == nwarps - 1) {
-          comb_cnt[fb] = 0;
-          last = 1;
+      int32_t x[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = 0;
+      if (fold_active) {
+        const uint32_t c = ((uint32_t)fbase >> 5) & 31u;  // same for all my bins (<= 16, aligned)
+        if (lb >= 2) {
+          const int4* H4 = reinterpret_cast<const int4*>(H);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (i < (1 << (lb - 2))) {
+              const int4 z = unswizzle4(H4[((fbase >> 2) + i) ^ (int)(c >> 2)], c);
+              x[4 * i] = z.x; x[4 * i + 1] = z.y; x[4 * i + 2] = z.z; x[4 * i + 3] = z.w;
+            }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (e < (1 << lb)) x[e] = H[key_swizzle((uint32_t)(fbase + e))];
         }
       }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        __threadfence_block();
-        const int b = p.b_begin + col_cta + f * ncol;
-        const int32_t r = (p.debug & 2) ? 0 : fold_combine(part, nwarps, lane);
-        const int w = block_width(p.cols, p.k, b);
-        const int sh = slot_shift(lane >> 1, lb);
-        if (!(lane & 1) && sh >= 0 && sh < w) emit(out, (int64_t)b * p.k + (w - 1 - sh), r, p.atomic_out != 0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hfree[fb]);  // release: my reads of the buffer are complete
+      int32_t a[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = 0;
+      int32_t X = 0;
+      if (FOLDPP) {
+#pragma unroll
+        for (int L = 0; L < 4; ++L) {
+          if (L < lb) {
+            const int cnt = 8 >> L;
+            int32_t odd = 0;
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt)
+              if (tt < cnt) {
+                odd += x[2 * tt + 1];
+                x[tt] = x[2 * tt] + x[2 * tt + 1];
+              }
+            a[L] = odd;
+          }
+        }
+        X = x[0];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+#pragma unroll
+          for (int L = 0; L < 4; ++L) a[L] += ((e >> L) & 1) ? x[e] : 0;
+          X += x[e];
+        }
       }
+      // slots 0-3: local bits (< lb); 4-8: lane bits; 9-13: warp bits (uniform per warp)
+#pragma unroll
+      for (int bit = 0; bit < 5; ++bit) a[4 + bit] = ((lane >> bit) & 1) ? X : 0;
+#pragma unroll
+      for (int bit = 0; bit < 5; ++bit) a[9 + bit] = ((warp >> bit) & 1) ? X : 0;
+      const int32_t r = reduce_scatter16(a, lane);  // lanes 2i, 2i+1: slot i summed over the warp
+      int32_t pv = 0;
+#pragma unroll
+      for (int i = 0; i < MAXNH; ++i)
+        if (i == fb) { pv = prev[i]; prev[i] = r; }
+      const int i = lane >> 1;
+      int sh = -1;
+      if (i < 4) sh = i < lb ? i : -1;
+      else if (i < 9) sh = lb + (i - 4);
+      else if (i < 14) sh = (i - 9) < wbits ? lb + 5 + (i - 9) : -1;
+      const int b = p.b_begin + col_cta + f * ncol;
+      const int w = block_width(p.cols, p.k, b);
+      if (!(lane & 1) && sh >= 0 && sh < w && r != pv) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)(r - pv));
     }
   }
 }
@@ -672,20 +593,14 @@ __global__ void naive_ternary_kernel(const int8_t* __restrict__ A, int64_t rows,
 // launchers
 // ------------------------------------------------------------------------------------
 
-template <int R, bool PP, typename OutT>
+template <bool PP, typename OutT>
 rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
-  auto kern = p.halves == 2 ? scatter_kernel<R, PP, true, OutT> : scatter_kernel<R, PP, false, OutT>;
+  auto kern = p.halves == 2 ? scatter_kernel<kScatterR, PP, true, OutT> : scatter_kernel<kScatterR, PP, false, OutT>;
   rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "scatter smem attribute");
   if (st != RSR_OK) return st;
   kern<<<grid, threads, smem, s>>>(p);
   return cuda_check(cudaGetLastError(), "scatter_kernel launch");
-}
-
-template <int R, typename OutT>
-rsr_status launch_scatter_r(const ScatterParams& p, bool pp, int grid, size_t smem, int threads, cudaStream_t s) {
-  return pp ? launch_scatter_t<R, true, OutT>(p, grid, smem, threads, s)
-            : launch_scatter_t<R, false, OutT>(p, grid, smem, threads, s);
 }
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out, rsr_dtype out_dtype, bool pp,
@@ -703,9 +618,8 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
   p.halves = d.halves;
   p.b_begin = b0;
   p.b_end = b1;
-  // rows per thread R (8 or 16), threads per CTA, row splits
-  const int R = d.rows > 8192 ? 16 : 8;
-  // power-of-two warp count: the distributed fold maps warp-index bits onto key bits
+  // R = 32 rows per thread; a power-of-two warp count (the fold maps warp-index bits onto key bits)
+  const int R = kScatterR;
   int threads = 32;
   while (threads < kScatterThreads && (int64_t)threads * R < d.rows) threads *= 2;
   p.rows_per_cta = threads * R;
@@ -713,32 +627,27 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
   p.atomic_out = p.n_splits > 1;
   const size_t slot_bytes = (size_t)d.halves * p.rows_per_cta * 2;
   const size_t max_smem = device_max_smem_optin();
-  const size_t hist1 = sizeof(int32_t) * ((size_t)1 << d.k);
-  const int nwarps_cta = threads / 32;
   auto need = [&](int st, int nh) {
-    return ((hist1 * nh + sizeof(int32_t) * nh * nwarps_cta * 17 + 127) & ~(size_t)127) + st * slot_bytes +
-           8 * (st + 2 * nh) + 4 * (st + nh) + 64;
+    return ((sizeof(int32_t) * ((((size_t)1 << d.k) * nh + 15) & ~(size_t)15) + 127) & ~(size_t)127) +
+           st * slot_bytes + 8 * ((threads / 32) * st + 2 * nh) + 64;
   };
-  {
-    const char* dbg = getenv("RSR_B200_DEBUG");
-    p.debug = dbg ? atoi(dbg) : 0;
-  }
-  // prefer >= 3 ring stages, then a second/third histogram buffer, then a 4th stage
+  // prefer >= 3 ring stages, then a third histogram buffer, then a 4th stage
   int stages = 0, nhist = 0;
-  const int cand[][2] = {{3, 3}, {3, 2}, {4, 2}, {2, 2}, {1, 2}};  // the deferred fold needs >= 2 buffers
+  const int cand[][2] = {{3, 3}, {3, 2}, {4, 2}, {2, 2}, {2, 3}, {1, 2}};  // the deferred fold needs 2..3 buffers
   for (auto& c : cand)
     if (need(c[0], c[1]) <= max_smem) { stages = c[0]; nhist = c[1]; break; }
   if (!stages) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: index slice does not fit in shared memory");
   if (stages == 3 && nhist == 3 && need(4, 3) <= max_smem) stages = 4;
   if (const char* e = getenv("RSR_B200_STAGES")) stages = atoi(e);  // diagnostics
-  if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::max(2, atoi(e));
+  if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::min(3, std::max(2, atoi(e)));
   p.stages = stages;
   p.nhist = nhist;
   const size_t smem = need(stages, nhist);
+  // small CTAs (few rows) share an SM
+  const int per_sm = std::max<int>(1, (int)std::min<size_t>(2048 / threads, (228u << 10) / (smem + 1024)));
   const int nblk = b1 - b0;
   const int sms = device_sm_count();
-  int ncol = std::max(1, std::min(nblk, sms / std::max(1, p.n_splits)));
-  if (ncol < 1) ncol = 1;
+  const int ncol = std::max(1, std::min(nblk, sms * per_sm / std::max(1, p.n_splits)));
   const int grid = ncol * p.n_splits;
   if (p.atomic_out) {
     const size_t esz = out_dtype == RSR_F64 ? 8 : 4;
@@ -748,10 +657,10 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
     if (st != RSR_OK) return st;
   }
   if (out_dtype == RSR_F64)
-    return R == 16 ? launch_scatter_r<16, double>(p, pp, grid, smem, threads, s)
-                   : launch_scatter_r<8, double>(p, pp, grid, smem, threads, s);
-  return R == 16 ? launch_scatter_r<16, int32_t>(p, pp, grid, smem, threads, s)
-                 : launch_scatter_r<8, int32_t>(p, pp, grid, smem, threads, s);
+    return pp ? launch_scatter_t<true, double>(p, grid, smem, threads, s)
+              : launch_scatter_t<false, double>(p, grid, smem, threads, s);
+  return pp ? launch_scatter_t<true, int32_t>(p, grid, smem, threads, s)
+            : launch_scatter_t<false, int32_t>(p, grid, smem, threads, s);
 }
 
 template <typename T>

@@ -102,7 +102,8 @@ __global__ void sort_blocks_kernel(rsr_index_desc d, uint32_t* __restrict__ gcnt
 
   for (int j = lane; j < nbk; j += 32) cnt[j] = 0;
   __syncwarp();
-  for (int64_t r = lane; r < rows; r += 32) atomicAdd(&cnt[key_swizzle(key[r])], 1u);
+  const unsigned kmask = (1u << d.k) - 1u;
+  for (int64_t r = lane; r < rows; r += 32) atomicAdd(&cnt[key_swizzle(key[r] & kmask)], 1u);
   __syncwarp();
   // Exclusive scan of cnt[0..nbk): lane owns a contiguous chunk.
   const int chunk = (nbk + 31) / 32;
@@ -125,7 +126,7 @@ __global__ void sort_blocks_kernel(rsr_index_desc d, uint32_t* __restrict__ gcnt
     const bool active = r < rows;
     const unsigned act = __ballot_sync(0xffffffffu, active);
     if (active) {
-      const unsigned kk = key_swizzle(key[r]);
+      const unsigned kk = key_swizzle(key[r] & kmask);
       const unsigned peers = __match_any_sync(act, kk);
       const int leader = __ffs(peers) - 1;
       uint32_t base = 0;

@@ -1,2 +1,3 @@
-for d in 0 1 2 3; do RSR_B200_DEBUG=$d python tools/prof_multiply.py --iters 3 | sed "s/^/debug=$d /"; done
-python tools/prof_multiply.py --iters 3 --variant rsr | sed "s/^/rsr /"
+python tools/prof_multiply.py --iters 3
+python tools/prof_multiply.py --iters 3 --variant rsr
+for c in llama4096 llama4096x14336 llama14336x4096; do python tools/prof_multiply.py --iters 3 --config $c; done
