@@ -57,8 +57,10 @@ typedef struct rsr_half_index {
                        j < 2^w, seg[2^w] = rows (indexer.py:274-276 incl. sentinel) */
   uint16_t* bucket; /* [nblocks][row_stride]: key of every row, MSB-first
                        (indexer.py:270 `_buckets`), as a device code:
-                       swz(key) = key ^ ((key >> 5) & 31) (bank swizzle, an involution);
-                       padding rows hold 0 */
+                       code = swz(key) << 2 for k <= 14 (swz(key) for k = 15, 16) where
+                       swz(key) = key ^ ((key >> 5) & 31) is a shared-memory bank swizzle
+                       (an involution) and << 2 makes the code the byte offset of the
+                       key's histogram word; padding rows hold 0 */
 } rsr_half_index;
 
 typedef struct rsr_index_desc {

@@ -103,11 +103,26 @@ __device__ __forceinline__ T warp_inclusive_scan(T x, int lane) {
 // bits.  An involution, so the same function encodes and decodes.
 __host__ __device__ __forceinline__ uint32_t key_swizzle(uint32_t j) { return j ^ ((j >> 5) & 31u); }
 
+// Device code of a bucket key stored in the index: the swizzled key, pre-multiplied by 4
+// (the byte offset of its histogram word) when k <= 14 so the scatter loop needs one ALU
+// op per key.  k = 15, 16 keep the plain swizzled key (u16 range).
+__host__ __device__ __forceinline__ uint32_t encode_key(uint32_t key, int k) {
+  return k <= 14 ? key_swizzle(key) << 2 : key_swizzle(key);
+}
+__host__ __device__ __forceinline__ uint32_t decode_key(uint32_t code, int k) {
+  return key_swizzle(k <= 14 ? (code >> 2) : code);
+}
+
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
   uint4 r;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
   return r;
 }
+
+// Programmatic dependent launch (PDL): wait until the preceding grid in the stream has
+// completed and flushed its memory; let the next grid start launching its CTAs.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Shared-memory reduction (no return value): ATOMS.ADD on sm_100.
 __device__ __forceinline__ void red_add_shared(uint32_t addr, int32_t v) {

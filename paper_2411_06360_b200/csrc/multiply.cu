@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
   constexpr int HALVES = TERNARY ? 2 : 1;
   constexpr int NG = R / 8;      // 8-row groups per lane
   constexpr int WROWS = 32 * R;  // rows per warp
-  constexpr int MAXNH = 3;
+  constexpr int MAXNH = 6;
   const int T = blockDim.x;
   const int nwarps = T >> 5;
   const int t = threadIdx.x;
@@ -174,22 +174,6 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
   const int fbase = (warp * 32 + lane) << lb;  // my first logical bin
   const bool fold_active = fbase < nbk;
 
-  // 1. issue the loads of my rows of v (they stay in registers for the whole launch)
-  int32_t vr[R];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    const int64_t row = wr0 + 256 * g + 8 * lane;
-    const int32_t* vp = p.v + row;
-    if (row + 8 <= p.rows && p.v_aligned) {
-      const int4 a = __ldg(reinterpret_cast<const int4*>(vp));
-      const int4 c = __ldg(reinterpret_cast<const int4*>(vp) + 1);
-      vr[8 * g + 0] = a.x; vr[8 * g + 1] = a.y; vr[8 * g + 2] = a.z; vr[8 * g + 3] = a.w;
-      vr[8 * g + 4] = c.x; vr[8 * g + 5] = c.y; vr[8 * g + 6] = c.z; vr[8 * g + 7] = c.w;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;
-    }
-  }
   // 2. start streaming this warp's keys of the first S units
   uint64_t policy = 0;
   if (lane == 0) {
@@ -210,8 +194,28 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
                       wbytes, &wfull[u], policy);
     }
   }
-  // 3. zero the histograms; a single-split launch owns its output columns: zero them here
+  // 3. zero the histograms
   for (int i = t; i < hist_words / 4; i += T) reinterpret_cast<int4*>(hist)[i] = make_int4(0, 0, 0, 0);
+  // Everything above only touched the (immutable) index; v and out may belong to the
+  // previous kernel in the stream (PDL): wait for it here.
+  grid_dependency_wait();
+  // 4. my rows of v, in registers for the whole launch
+  int32_t vr[R];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const int64_t row = wr0 + 256 * g + 8 * lane;
+    const int32_t* vp = p.v + row;
+    if (row + 8 <= p.rows && p.v_aligned) {
+      const int4 a = __ldg(reinterpret_cast<const int4*>(vp));
+      const int4 c = __ldg(reinterpret_cast<const int4*>(vp) + 1);
+      vr[8 * g + 0] = a.x; vr[8 * g + 1] = a.y; vr[8 * g + 2] = a.z; vr[8 * g + 3] = a.w;
+      vr[8 * g + 4] = c.x; vr[8 * g + 5] = c.y; vr[8 * g + 6] = c.z; vr[8 * g + 7] = c.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;
+    }
+  }
+  // 5. a single-split launch owns its output columns: zero them here
   if (!p.atomic_out)
     for (int i = t; i < nunits * p.k; i += T) {
       const int b = p.b_begin + col_cta + (i / p.k) * ncol;
@@ -237,6 +241,7 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
   }
 
   for (int u = 0; u <= nunits; ++u) {
+    if (u + 1 == nunits) grid_launch_dependents();  // the next grid may start its prologue on freed SMs
     if (u < nunits) {
       const int slot = u % S;
       const int hb = u % NH;
@@ -263,8 +268,8 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
-              red_add_shared(Hs + ((w4[e] & 0xffffu) << 2), h ? -a : a);
-              red_add_shared(Hs + ((w4[e] >> 16) << 2), h ? -c : c);
+              red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
+              red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
             }
           }
         } else {  // rows past the end of the matrix were never copied: skip them
@@ -275,8 +280,8 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
-              if (row + 2 * e < p.rows) red_add_shared(Hs + ((w4[e] & 0xffffu) << 2), h ? -a : a);
-              if (row + 2 * e + 1 < p.rows) red_add_shared(Hs + ((w4[e] >> 16) << 2), h ? -c : c);
+              if (row + 2 * e < p.rows) red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
+              if (row + 2 * e + 1 < p.rows) red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
             }
           }
         }
@@ -593,14 +598,33 @@ __global__ void naive_ternary_kernel(const int8_t* __restrict__ A, int64_t rows,
 // launchers
 // ------------------------------------------------------------------------------------
 
+// Programmatic dependent launch on by default (RSR_B200_PDL=0 disables it).
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RSR_B200_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 template <bool PP, typename OutT>
 rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
   auto kern = p.halves == 2 ? scatter_kernel<kScatterR, PP, true, OutT> : scatter_kernel<kScatterR, PP, false, OutT>;
   rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "scatter smem attribute");
   if (st != RSR_OK) return st;
-  kern<<<grid, threads, smem, s>>>(p);
-  return cuda_check(cudaGetLastError(), "scatter_kernel launch");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_check(cudaLaunchKernelEx(&cfg, kern, p), "scatter_kernel launch");
 }
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out, rsr_dtype out_dtype, bool pp,
@@ -639,7 +663,7 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
   if (!stages) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: index slice does not fit in shared memory");
   if (stages == 3 && nhist == 3 && need(4, 3) <= max_smem) stages = 4;
   if (const char* e = getenv("RSR_B200_STAGES")) stages = atoi(e);  // diagnostics
-  if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::min(3, std::max(2, atoi(e)));
+  if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::min(6, std::max(2, atoi(e)));
   p.stages = stages;
   p.nhist = nhist;
   const size_t smem = need(stages, nhist);

@@ -58,8 +58,8 @@ __global__ void __launch_bounds__(kKeyThreads) keys_ternary_kernel(const int8_t*
       kn = (kn << 1) | (unsigned)(x == -1);
     }
     int64_t o = (int64_t)(b0 + bl) * row_stride + r0 + r;
-    kpos[o] = (uint16_t)key_swizzle(kp);
-    kneg[o] = (uint16_t)key_swizzle(kn);
+    kpos[o] = (uint16_t)encode_key(kp, k);
+    kneg[o] = (uint16_t)encode_key(kn, k);
   }
 }
 
@@ -77,7 +77,7 @@ __global__ void keys_binary_kernel(const uint8_t* __restrict__ bits, int64_t ldb
       int64_t cc = c0 + c;
       key = (key << 1) | ((row[cc >> 3] >> (7 - (cc & 7))) & 1u);
     }
-    keys[(int64_t)b * row_stride + r] = (uint16_t)key_swizzle(key);
+    keys[(int64_t)b * row_stride + r] = (uint16_t)encode_key(key, k);
   }
 }
 
@@ -102,8 +102,7 @@ __global__ void sort_blocks_kernel(rsr_index_desc d, uint32_t* __restrict__ gcnt
 
   for (int j = lane; j < nbk; j += 32) cnt[j] = 0;
   __syncwarp();
-  const unsigned kmask = (1u << d.k) - 1u;
-  for (int64_t r = lane; r < rows; r += 32) atomicAdd(&cnt[key_swizzle(key[r] & kmask)], 1u);
+  for (int64_t r = lane; r < rows; r += 32) atomicAdd(&cnt[decode_key(key[r], d.k)], 1u);
   __syncwarp();
   // Exclusive scan of cnt[0..nbk): lane owns a contiguous chunk.
   const int chunk = (nbk + 31) / 32;
@@ -126,7 +125,7 @@ __global__ void sort_blocks_kernel(rsr_index_desc d, uint32_t* __restrict__ gcnt
     const bool active = r < rows;
     const unsigned act = __ballot_sync(0xffffffffu, active);
     if (active) {
-      const unsigned kk = key_swizzle(key[r] & kmask);
+      const unsigned kk = decode_key(key[r], d.k);
       const unsigned peers = __match_any_sync(act, kk);
       const int leader = __ffs(peers) - 1;
       uint32_t base = 0;
