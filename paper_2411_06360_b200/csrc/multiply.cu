@@ -389,121 +389,168 @@ struct GatherParams {
   void* out;
   int64_t rows, cols, row_stride, seg_stride;
   int k, halves, b_begin, b_end;
-  int perm_bytes, v_in_smem, warps_per_cta;
+  int perm_bytes, v_in_smem, seg_in_smem;
 };
+
+constexpr int kGatherWarps = 8;
+constexpr int kPermAhead = 4;  // perm windows in flight per warp (16-byte loads, registers)  // one CTA works on one column block at a time
 
 template <typename T>
 __device__ __forceinline__ T vload(const T* vs, const T* vg, uint32_t row, bool smem) {
   return smem ? vs[row] : __ldg(vg + row);
 }
 
+// One CTA per column block at a time (persistent over blocks).  The 8 warps split the block's
+// sorted positions: (half, part) = (warp / P, warp % P), P = 8 / halves contiguous position
+// ranges per half.  Per 256-position window a warp gathers v[perm[p]] from shared memory (8
+// positions per lane, perm prefetched one window ahead), forms window-local prefix sums with a
+// warp scan, and every bucket boundary j (position seg[j], seg staged in shared memory) adds
+// its prefix with the RSR++ telescoping coefficients bit_s(j-1) - bit_s(j) — the pairwise
+// compaction of Alg. 3 applied to prefix sums, ~2 adds per bucket — or, for variant "rsr",
+// forms the segment sum and adds it to every column whose bit is set.  The bucket open at a
+// range / window end contributes the remaining tail.  Linear, so the warps' partial column
+// sums are combined in a fixed order: deterministic, no float atomics.
 template <typename T, bool FOLDPP>
-__global__ void __launch_bounds__(512) gather_kernel(const GatherParams p) {
+__global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  T* pbuf_all = reinterpret_cast<T*>(smem);
-  T* pbuf = pbuf_all + wib * 256;
-  T* vs = pbuf_all + p.warps_per_cta * 256;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg_words = p.seg_in_smem ? (int)((p.seg_stride + 3) & ~3) : 0;
+  uint32_t* segs = reinterpret_cast<uint32_t*>(smem);                       // [2][seg_words]
+  T* pbuf_all = reinterpret_cast<T*>(segs + 2 * seg_words);                  // [8][256]
+  T* pbuf = pbuf_all + warp * 256;
+  T* part = pbuf_all + kGatherWarps * 256;                                   // [8][16]
+  T* vs = part + kGatherWarps * 16;
   const T* vg = reinterpret_cast<const T*>(p.v);
   const bool vsm = p.v_in_smem != 0;
   if (vsm) {
-    const int64_t n = p.rows;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) vs[i] = vg[i];
-    __syncthreads();
+    for (int64_t i = threadIdx.x; i < p.rows; i += blockDim.x) vs[i] = vg[i];
   }
-  const int nwarps_total = gridDim.x * p.warps_per_cta;
-  const int gw = blockIdx.x * p.warps_per_cta + wib;
   T* out = reinterpret_cast<T*>(p.out);
+  const int P = kGatherWarps / p.halves;  // position ranges per half
+  const int h = warp / P, part_i = warp % P;
+  const int64_t plen = ((p.rows + P - 1) / P + 255) / 256 * 256;  // window-aligned range length
+  const int64_t P0 = (int64_t)part_i * plen;
+  const int64_t P1 = std::min<int64_t>(p.rows, P0 + plen);
   const uint32_t* seg0 = p.seg[0];
   const uint32_t* seg1 = p.seg[1];
-  const void* perm0 = p.perm[0];
-  const void* perm1 = p.perm[1];
+  const void* perm_g = h ? p.perm[1] : p.perm[0];
+  const T sgn = h ? T(-1) : T(1);
 
-  for (int b = p.b_begin + gw; b < p.b_end; b += nwarps_total) {
+  for (int b = p.b_begin + blockIdx.x; b < p.b_end; b += gridDim.x) {
     const int w = block_width(p.cols, p.k, b);
     const int nbk = 1 << w;
+    __syncthreads();  // previous block's segs / part are no longer read
+    if (p.seg_in_smem)
+      for (int i = threadIdx.x; i < p.halves * (nbk + 1); i += blockDim.x) {
+        const int hh = i / (nbk + 1), j = i % (nbk + 1);
+        segs[hh * seg_words + j] = (hh ? seg1 : seg0)[(int64_t)b * p.seg_stride + j];
+      }
+    __syncthreads();
+    const uint32_t* seg = p.seg_in_smem ? segs + h * seg_words : (h ? seg1 : seg0) + (int64_t)b * p.seg_stride;
     T acc[kMaxK];
 #pragma unroll
     for (int s = 0; s < kMaxK; ++s) acc[s] = T(0);
-    for (int h = 0; h < p.halves; ++h) {
-      const T sgn = h ? T(-1) : T(1);
-      const uint32_t* seg = (h ? seg1 : seg0) + (int64_t)b * p.seg_stride;
-      const void* permh = h ? perm1 : perm0;
-      const uint16_t* perm16 = reinterpret_cast<const uint16_t*>(permh) + (int64_t)b * p.row_stride;
-      const uint32_t* perm32 = reinterpret_cast<const uint32_t*>(permh) + (int64_t)b * p.row_stride;
-      int jcur = 1;      // next boundary to consume (boundary j sits at position seg[j])
-      T carry = T(0);    // RSR: partial sum of the bucket open at the window start
-      for (int64_t w0 = 0; w0 < p.rows; w0 += 256) {
-        const int E = (int)std::min<int64_t>(256, p.rows - w0);
+    if (P0 < P1) {
+      // first boundary after P0: jcur = 1 + #{j in [1, nbk] : seg[j] <= P0}
+      int lo = 1, hi = nbk + 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int64_t)seg[mid] <= P0) lo = mid + 1; else hi = mid;
+      }
+      int jcur = (P0 == 0) ? 1 : lo;
+      T carry = T(0);
+      const uint16_t* perm16 = reinterpret_cast<const uint16_t*>(perm_g) + (int64_t)b * p.row_stride;
+      const uint32_t* perm32 = reinterpret_cast<const uint32_t*>(perm_g) + (int64_t)b * p.row_stride;
+      // perm stream: kPermAhead windows of 16-byte loads in flight (register ring)
+      auto load_perm = [&](int64_t w0, uint4 (&q)[2]) {
         const int64_t pos0 = w0 + 8 * lane;
+        q[0] = q[1] = make_uint4(0, 0, 0, 0);
+        if (pos0 < P1) {
+          if (p.perm_bytes == 2) {
+            q[0] = ld_nc_v4(perm16 + pos0);
+          } else {
+            q[0] = ld_nc_v4(perm32 + pos0);
+            q[1] = ld_nc_v4(perm32 + pos0 + 4);
+          }
+        }
+      };
+      uint4 ring[kPermAhead][2];
+#pragma unroll
+      for (int i = 0; i < kPermAhead; ++i) load_perm(P0 + 256 * i, ring[i]);
+      int rslot = 0;
+      for (int64_t w0 = P0; w0 < P1; w0 += 256) {
+        const int E = (int)std::min<int64_t>(256, P1 - w0);
+        const int64_t pos0 = w0 + 8 * lane;
+        uint4 q0 = ring[0][0], q1 = ring[0][1];
+#pragma unroll
+        for (int i = 1; i < kPermAhead; ++i)
+          if (i == rslot) { q0 = ring[i][0]; q1 = ring[i][1]; }
         uint32_t rowsel[8];
         if (p.perm_bytes == 2) {
-          uint4 q = make_uint4(0, 0, 0, 0);
-          if (pos0 < p.row_stride) q = ld_nc_v4(perm16 + pos0);
-          rowsel[0] = q.x & 0xffffu; rowsel[1] = q.x >> 16;
-          rowsel[2] = q.y & 0xffffu; rowsel[3] = q.y >> 16;
-          rowsel[4] = q.z & 0xffffu; rowsel[5] = q.z >> 16;
-          rowsel[6] = q.w & 0xffffu; rowsel[7] = q.w >> 16;
+          rowsel[0] = q0.x & 0xffffu; rowsel[1] = q0.x >> 16; rowsel[2] = q0.y & 0xffffu; rowsel[3] = q0.y >> 16;
+          rowsel[4] = q0.z & 0xffffu; rowsel[5] = q0.z >> 16; rowsel[6] = q0.w & 0xffffu; rowsel[7] = q0.w >> 16;
         } else {
-          uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-          if (pos0 < p.row_stride) { q0 = ld_nc_v4(perm32 + pos0); q1 = ld_nc_v4(perm32 + pos0 + 4); }
           rowsel[0] = q0.x; rowsel[1] = q0.y; rowsel[2] = q0.z; rowsel[3] = q0.w;
           rowsel[4] = q1.x; rowsel[5] = q1.y; rowsel[6] = q1.z; rowsel[7] = q1.w;
         }
         T x[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = (pos0 + e < p.rows) ? vload(vs, vg, rowsel[e], vsm) : T(0);
+        for (int e = 0; e < 8; ++e) x[e] = (pos0 + e < P1) ? vload(vs, vg, rowsel[e], vsm) : T(0);
+        {  // refill this ring slot with the window kPermAhead ahead
+          uint4 nq[2];
+          load_perm(w0 + 256 * kPermAhead, nq);
+#pragma unroll
+          for (int i = 0; i < kPermAhead; ++i)
+            if (i == rslot) { ring[i][0] = nq[0]; ring[i][1] = nq[1]; }
+          rslot = rslot + 1 == kPermAhead ? 0 : rslot + 1;
+        }
 #pragma unroll
         for (int e = 1; e < 8; ++e) x[e] += x[e - 1];
         const T incl = warp_inclusive_scan(x[7], lane);
         const T base = incl - x[7];
         const T total = __shfl_sync(0xffffffffu, incl, 31);
+        // transposed prefix buffer: position 8*lane + e lives at e*32 + lane (conflict-free stores)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) pbuf[8 * lane + e] = base + x[e];
+        for (int e = 0; e < 8; ++e) pbuf[e * 32 + lane] = base + x[e];
         __syncwarp();
-        // consume the boundaries that fall in (w0, w0 + E] (window 0: [0, E])
-        int last_in = -1;  // lane index of the last included boundary in the final batch
+        int last_in = -1;
         T p_last = T(0);
         while (true) {
           const int jj = jcur + lane;
           const int64_t sj = jj <= nbk ? (int64_t)seg[jj] : INT64_MAX;
           const bool in = sj <= w0 + E;
-          const unsigned bal = __ballot_sync(0xffffffffu, in);
-          const int cnt = __popc(bal);
-          T P = T(0);
+          const int cnt = __popc(__ballot_sync(0xffffffffu, in));
+          T Pv = T(0);
           if (in) {
-            const int q = (int)(sj - w0);
-            P = q ? pbuf[q - 1] : T(0);
+            const int q = (int)(sj - w0) - 1;
+            Pv = q >= 0 ? pbuf[((q & 7) << 5) | (q >> 3)] : T(0);
           }
           if (FOLDPP) {
             if (in) {
-              // boundary j closes bucket j-1 and opens bucket j: coefficient bit_s(j-1) - bit_s(j)
-              const int tz = __ffs(jj) - 1;
+              const int tz = __ffs(jj) - 1;  // boundary j closes bucket j-1 and opens bucket j
 #pragma unroll
-              for (int s = 0; s < kMaxK; ++s) acc[s] += (s < tz) ? sgn * P : ((s == tz) ? -sgn * P : T(0));
+              for (int s = 0; s < kMaxK; ++s) acc[s] += (s < tz) ? sgn * Pv : ((s == tz) ? -sgn * Pv : T(0));
             }
           } else {
-            // segment sum of bucket jj-1 = P(jj) - P(previous boundary) (+ carry for the first)
-            T prevP = __shfl_up_sync(0xffffffffu, P, 1);
+            const T prevP = __shfl_up_sync(0xffffffffu, Pv, 1);
             if (in) {
-              const T uj = (lane == 0) ? carry + P : P - prevP;
+              const T uj = (lane == 0) ? carry + Pv : Pv - prevP;
               const int j = jj - 1;
 #pragma unroll
               for (int s = 0; s < kMaxK; ++s) acc[s] += ((j >> s) & 1) ? sgn * uj : T(0);
             }
             if (cnt > 0) {
-              p_last = __shfl_sync(0xffffffffu, P, cnt - 1);
+              p_last = __shfl_sync(0xffffffffu, Pv, cnt - 1);
               carry = T(0);
               last_in = cnt - 1;
             }
           }
           jcur += cnt;
           if (cnt < 32) break;
-          if (!FOLDPP) carry = T(0) - p_last;  // next batch's first boundary continues from p_last
+          if (!FOLDPP) carry = T(0) - p_last;
         }
         if (FOLDPP) {
-          // bucket open at the window end contributes the whole window tail: bit_s(g) * total
-          const int g = jcur - 1;
+          const int g = jcur - 1;  // bucket open at the window end: its tail is the window total
           if (lane == 0) {
 #pragma unroll
             for (int s = 0; s < kMaxK; ++s) acc[s] += ((g >> s) & 1) ? sgn * total : T(0);
@@ -513,17 +560,23 @@ __global__ void __launch_bounds__(512) gather_kernel(const GatherParams p) {
         }
         __syncwarp();
       }
-    }
-    // reduce the per-lane column accumulators; lane s writes column w-1-s
-    T mine = T(0);
+      if (!FOLDPP) {
+        // the bucket still open at the range end gets the carried tail
+        const int g = jcur - 1;
+        if (lane == 0 && P1 < p.rows) {
 #pragma unroll
-    for (int s = 0; s < kMaxK; ++s) {
-      if (s < w) {
-        T r = warp_sum(acc[s]);
-        if (lane == s) mine = r;
+          for (int s = 0; s < kMaxK; ++s) acc[s] += ((g >> s) & 1) ? sgn * carry : T(0);
+        }
       }
     }
-    if (lane < w) out[(int64_t)b * p.k + (w - 1 - lane)] = mine;
+    const T r = reduce_scatter16(acc, lane);  // lanes 2s, 2s+1: warp total of column shift s
+    if (!(lane & 1)) part[warp * 16 + (lane >> 1)] = r;
+    __syncthreads();
+    if (warp == 0 && lane < w) {
+      T sum = T(0);
+      for (int ww = 0; ww < kGatherWarps; ++ww) sum += part[ww * 16 + lane];
+      out[(int64_t)b * p.k + (w - 1 - lane)] = sum;
+    }
   }
 }
 
@@ -707,20 +760,21 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
   p.b_end = b1;
   p.perm_bytes = d.perm_bytes;
   const size_t max_smem = device_max_smem_optin();
-  const int nblk = b1 - b0;
-  int wpc = 16;
+  const size_t pbuf_bytes = sizeof(T) * (kGatherWarps * 256 + kGatherWarps * 16);
+  p.seg_in_smem = sizeof(uint32_t) * 2 * (size_t)((d.seg_stride + 3) & ~3) + pbuf_bytes <= (96u << 10);
+  const size_t seg_words = p.seg_in_smem ? (size_t)((d.seg_stride + 3) & ~3) : 0;
+  const size_t fixed = sizeof(uint32_t) * 2 * seg_words + pbuf_bytes;
   const size_t vbytes = sizeof(T) * (size_t)d.rows;
-  p.v_in_smem = (vbytes + sizeof(T) * 256 * wpc) <= max_smem;
-  p.warps_per_cta = wpc;
-  const size_t smem = sizeof(T) * 256 * wpc + (p.v_in_smem ? vbytes : 0);
-  const int ctas_per_sm = p.v_in_smem ? std::max<int>(1, (int)std::min<size_t>(4, (228u << 10) / (smem + 1024))) : 2;
-  const int want = (nblk + wpc - 1) / wpc;
-  const int grid = std::max(1, std::min(want, device_sm_count() * ctas_per_sm));
+  p.v_in_smem = fixed + vbytes <= max_smem;
+  const size_t smem = fixed + (p.v_in_smem ? vbytes : 0);
+  const int per_sm = std::max<int>(1, (int)std::min<size_t>(4, (228u << 10) / (smem + 1024)));
+  const int nblk = b1 - b0;
+  const int grid = std::max(1, std::min(nblk, device_sm_count() * per_sm));
   auto kern = pp ? gather_kernel<T, true> : gather_kernel<T, false>;
   rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "gather smem attribute");
   if (st != RSR_OK) return st;
-  kern<<<grid, 32 * wpc, smem, s>>>(p);
+  kern<<<grid, kGatherWarps * 32, smem, s>>>(p);
   return cuda_check(cudaGetLastError(), "gather_kernel launch");
 }
 

@@ -1,2 +1,3 @@
 python tools/prof_multiply.py --iters 3
-RSR_B200_PDL=0 python tools/prof_multiply.py --iters 3
+for dt in float32 int32 float64; do python tools/prof_multiply.py --iters 3 --form gather --dtype $dt; done
+python tools/prof_multiply.py --iters 3 --form gather --dtype float32 --variant rsr
