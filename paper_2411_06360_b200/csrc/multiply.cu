@@ -40,6 +40,7 @@ namespace {
 
 constexpr int kScatterThreads = 512;  // x kScatterR rows per thread = 16384 rows per CTA
 constexpr int kScatterR = 32;
+constexpr int kFoldWarps = 4;  // dedicated fold warps per CTA
 constexpr int kMaxK = 16;
 
 // =====================================================================================
@@ -81,6 +82,7 @@ struct ScatterParams {
   int k, halves, b_begin, b_end;
   int rows_per_cta, n_splits, stages, atomic_out, nhist;
   int v_aligned;
+  int scatter_warps;
 };
 
 template <typename OutT>
@@ -107,36 +109,33 @@ __device__ __forceinline__ int4 unswizzle4(int4 q, uint32_t c) {
   return q;
 }
 
-// Persistent CTA (up to 16 warps, one CTA per SM at n >= 8192), every warp scatters and folds.
-//  * Lane l of warp w owns rows w*32R + 256g + 8l + e (g < R/8, e < 8) of the CTA's row
-//    slice: their v values live in registers for the whole launch.  Each warp streams its
-//    rows' keys of every column block through a private S-slot shared-memory ring with 1-D
-//    TMA bulk copies (lane 0 issues, per-warp mbarriers) and refills a slot as soon as it
-//    has read it.  Key reads are conflict-free 16-byte loads (512 contiguous bytes per warp
-//    instruction) and are software-pipelined one half-unit ahead, so the shared-memory
-//    reductions of one half hide the load latency of the next.
+// Persistent CTA (one per SM at n >= 8192): up to 16 SCATTER warps + kFoldWarps FOLD warps.
+//  * Scatter warp w, lane l owns rows w*32R + 256g + 8l + e (g < R/8, e < 8) of the CTA's row
+//    slice: their v values live in registers for the whole launch.  Each scatter warp streams
+//    its rows' key codes of every column block through a private S-slot shared-memory ring
+//    with 1-D TMA bulk copies (lane 0 issues, per-warp mbarriers) and refills a slot as soon
+//    as it has read it.  Key reads are conflict-free 16-byte loads, software-pipelined one
+//    half-block ahead, so the reductions of one half hide the load latency of the next.
 //  * Both halves of a ternary index scatter into ONE 2^k-bin histogram (+v for the positive
 //    key, -v for the negative key): the fold is linear, so fold(u+ - u-) is exactly the
 //    reference's `pos - neg` (kernels.py:206) in integer arithmetic.
-//  * Distributed fold: after scattering unit u, every warp folds its own 1/nwarps slice of
-//    unit u-1's histogram.  Bins j = (warp*32 + lane) * 2^lb + e: the e bits are folded in
-//    registers (RSR++ pairwise compaction, kernels.py:74-91, or the dense RSR product,
-//    kernels.py:63-71), lane bits by one warp reduce-scatter, warp bits are uniform; each
-//    warp then adds its share of the block's w outputs with one global reduction.
-//  * Histogram buffers are never zeroed: unit u adds into buffer u % NH on top of unit
-//    u - NH; each warp keeps its previous slice fold per buffer and adds only the
-//    difference (exact modulo 2^32).  Barriers: hfull[b] (all warps scattered) before the
-//    fold reads, hfree[b] (all warps read their slice) before the buffer is reused.
+//  * The fold warps never scatter, so folding overlaps the scatter warps' reductions instead
+//    of stalling them: for every block they wait on hfull (all scatter warps done), each
+//    reads its quarter of the histogram (RSR++ pairwise compaction of the lane-local bits,
+//    kernels.py:74-91, or the dense RSR product, kernels.py:63-71), reduces the lane bits with
+//    REDUX, and adds its share of the k outputs with global reductions; then arrives on hfree.
+//  * Histogram buffers are never zeroed: block u adds into buffer u % NH on top of block
+//    u - NH; each fold lane keeps its previous fold of the buffer and adds the difference
+//    (exact modulo 2^32).
 template <int R, bool FOLDPP, bool TERNARY, typename OutT>
-__global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const ScatterParams p) {
+__global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
   static_assert(R % 8 == 0 && R * kScatterThreads <= 16384, "rows per CTA");
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int HALVES = TERNARY ? 2 : 1;
   constexpr int NG = R / 8;      // 8-row groups per lane
   constexpr int WROWS = 32 * R;  // rows per warp
-  constexpr int MAXNH = 6;
-  const int T = blockDim.x;
-  const int nwarps = T >> 5;
+  constexpr int MAXNH = 4;
+  const int nwarps = p.scatter_warps;  // scatter warps; fold warps follow them
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const int nbk = 1 << p.k;
@@ -145,9 +144,7 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
   const int hist_words = (NH * nbk + 15) & ~15;
   int32_t* hist = reinterpret_cast<int32_t*>(smem);  // [NH][nbk]
   uint16_t* ring_all = reinterpret_cast<uint16_t*>(smem + ((sizeof(int32_t) * hist_words + 127) & ~(size_t)127));
-  uint16_t* ring = ring_all + (size_t)warp * S * HALVES * WROWS;  // this warp's [S][HALVES][WROWS]
   uint64_t* wfull_all = reinterpret_cast<uint64_t*>(ring_all + (size_t)nwarps * S * HALVES * WROWS);
-  uint64_t* wfull = wfull_all + warp * S;
   uint64_t* hfull = wfull_all + nwarps * S;
   uint64_t* hfree = hfull + NH;
 
@@ -157,32 +154,20 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
   const int64_t r0 = (int64_t)split * p.rows_per_cta;
   const int nblk = p.b_end - p.b_begin;
   const int nunits = col_cta < nblk ? (nblk - col_cta + ncol - 1) / ncol : 0;
-  const int64_t wr0 = r0 + (int64_t)warp * WROWS;  // first row of this warp
-  const int wcopy = (int)std::max<int64_t>(0, std::min<int64_t>(WROWS, p.row_stride - wr0));  // multiple of 8
-  const uint32_t wbytes = (uint32_t)wcopy * 2u;
-  // rows of my groups: wr0 + 256g + 8l + e; all valid iff the last group's 8 rows are < rows
-  const bool all_valid = wr0 + 256 * (NG - 1) + 8 * lane + 8 <= p.rows;
   const uint16_t* key0 = p.key[0];
   const uint16_t* key1 = p.key[1];
-  const uint32_t hist_s = smem_u32(hist);
-  const uint32_t ring_s = smem_u32(ring);
   OutT* out = reinterpret_cast<OutT*>(p.out);
-  // fold geometry: 2^lb bins per lane, warp index bits start at bit lb + 5
-  const int wbits = 31 - __clz(nwarps);
-  int lb = p.k - 5 - wbits;
-  if (lb < 0) lb = 0;
-  const int fbase = (warp * 32 + lane) << lb;  // my first logical bin
-  const bool fold_active = fbase < nbk;
+  const bool is_fold = warp >= nwarps;
 
-  // 2. start streaming this warp's keys of the first S units
+  // ---- prologue (index only: may overlap the previous kernel under PDL) ----
+  uint16_t* ring = ring_all + (size_t)(is_fold ? 0 : warp) * S * HALVES * WROWS;  // my [S][HALVES][WROWS]
+  uint64_t* wfull = wfull_all + (is_fold ? 0 : warp) * S;
+  const int64_t wr0 = r0 + (int64_t)warp * WROWS;  // first row of this (scatter) warp
+  const int wcopy = is_fold ? 0 : (int)std::max<int64_t>(0, std::min<int64_t>(WROWS, p.row_stride - wr0));
+  const uint32_t wbytes = (uint32_t)wcopy * 2u;
   uint64_t policy = 0;
-  if (lane == 0) {
+  if (lane == 0 && !is_fold) {
     for (int s = 0; s < S; ++s) mbar_init(&wfull[s], 1);
-    if (warp == 0)
-      for (int h = 0; h < NH; ++h) {
-        mbar_init(&hfull[h], nwarps);
-        mbar_init(&hfree[h], nwarps);
-      }
     fence_mbar_init();
     policy = l2_evict_first_policy();
     for (int u = 0; u < S && u < nunits; ++u) {
@@ -194,63 +179,63 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
                       wbytes, &wfull[u], policy);
     }
   }
-  // 3. zero the histograms
-  for (int i = t; i < hist_words / 4; i += T) reinterpret_cast<int4*>(hist)[i] = make_int4(0, 0, 0, 0);
-  // Everything above only touched the (immutable) index; v and out may belong to the
-  // previous kernel in the stream (PDL): wait for it here.
-  grid_dependency_wait();
-  // 4. my rows of v, in registers for the whole launch
-  int32_t vr[R];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    const int64_t row = wr0 + 256 * g + 8 * lane;
-    const int32_t* vp = p.v + row;
-    if (row + 8 <= p.rows && p.v_aligned) {
-      const int4 a = __ldg(reinterpret_cast<const int4*>(vp));
-      const int4 c = __ldg(reinterpret_cast<const int4*>(vp) + 1);
-      vr[8 * g + 0] = a.x; vr[8 * g + 1] = a.y; vr[8 * g + 2] = a.z; vr[8 * g + 3] = a.w;
-      vr[8 * g + 4] = c.x; vr[8 * g + 5] = c.y; vr[8 * g + 6] = c.z; vr[8 * g + 7] = c.w;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;
+  if (t == 0) {
+    for (int h = 0; h < NH; ++h) {
+      mbar_init(&hfull[h], nwarps);
+      mbar_init(&hfree[h], kFoldWarps);
     }
+    fence_mbar_init();
   }
-  // 5. a single-split launch owns its output columns: zero them here
-  if (!p.atomic_out)
-    for (int i = t; i < nunits * p.k; i += T) {
+  for (int i = t; i < hist_words / 4; i += blockDim.x) reinterpret_cast<int4*>(hist)[i] = make_int4(0, 0, 0, 0);
+  // v and out may belong to the previous kernel in the stream: wait for it here (PDL)
+  grid_dependency_wait();
+  if (!p.atomic_out)  // a single-split launch owns its output columns
+    for (int i = t; i < nunits * p.k; i += blockDim.x) {
       const int b = p.b_begin + col_cta + (i / p.k) * ncol;
       const int c = i % p.k;
       if (c < block_width(p.cols, p.k, b)) out[(int64_t)b * p.k + c] = (OutT)0;
     }
-  __syncthreads();
 
-  int32_t prev[MAXNH];  // my previous slice fold of each buffer (lanes 2s: column shift s)
+  if (!is_fold) {
+    // =========================== scatter warps ===========================
+    const bool all_valid = wr0 + 256 * (NG - 1) + 8 * lane + 8 <= p.rows;
+    const uint32_t hist_s = smem_u32(hist);
+    const uint32_t ring_s = smem_u32(ring);
+    int32_t vr[R];
 #pragma unroll
-  for (int i = 0; i < MAXNH; ++i) prev[i] = 0;
-
-  // key loads of one half-unit: NG conflict-free 16-byte loads
-  auto load_keys = [&](int slot, int h, uint4 (&q)[NG]) {
-    const uint32_t base = ring_s + (uint32_t)(((slot * HALVES + h) * WROWS + 8 * lane) * 2);
+    for (int g = 0; g < NG; ++g) {
+      const int64_t row = wr0 + 256 * g + 8 * lane;
+      const int32_t* vp = p.v + row;
+      if (row + 8 <= p.rows && p.v_aligned) {
+        const int4 a = __ldg(reinterpret_cast<const int4*>(vp));
+        const int4 c = __ldg(reinterpret_cast<const int4*>(vp) + 1);
+        vr[8 * g + 0] = a.x; vr[8 * g + 1] = a.y; vr[8 * g + 2] = a.z; vr[8 * g + 3] = a.w;
+        vr[8 * g + 4] = c.x; vr[8 * g + 5] = c.y; vr[8 * g + 6] = c.z; vr[8 * g + 7] = c.w;
+      } else {
 #pragma unroll
-    for (int g = 0; g < NG; ++g) q[g] = ld_shared_v4(base + (uint32_t)(g * 512));
-  };
-  uint4 q[NG];
-  if (nunits > 0) {
-    mbar_wait(&wfull[0], 0);
-    load_keys(0, 0, q);
-  }
-
-  for (int u = 0; u <= nunits; ++u) {
-    if (u + 1 == nunits) grid_launch_dependents();  // the next grid may start its prologue on freed SMs
-    if (u < nunits) {
+        for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;
+      }
+    }
+    __syncthreads();
+    auto load_keys = [&](int slot, int h, uint4 (&q)[NG]) {
+      const uint32_t base = ring_s + (uint32_t)(((slot * HALVES + h) * WROWS + 8 * lane) * 2);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) q[g] = ld_shared_v4(base + (uint32_t)(g * 512));
+    };
+    uint4 q[NG];
+    if (nunits > 0) {
+      mbar_wait(&wfull[0], 0);
+      load_keys(0, 0, q);
+    }
+    for (int u = 0; u < nunits; ++u) {
+      if (u + 1 == nunits) grid_launch_dependents();  // the next grid may start its prologue on freed SMs
       const int slot = u % S;
       const int hb = u % NH;
       const uint32_t Hs = hist_s + (uint32_t)(hb * nbk) * 4u;
       if (u >= NH) mbar_wait(&hfree[hb], (uint32_t)(((u / NH) - 1) & 1));
 #pragma unroll
       for (int h = 0; h < HALVES; ++h) {
-        // prefetch the next half-unit's keys before issuing this half's reductions
-        uint4 qn[NG];
+        uint4 qn[NG];  // next half-block's keys, loaded before this half's reductions
         if (h + 1 < HALVES) {
           load_keys(slot, h + 1, qn);
         } else if (u + 1 < nunits) {
@@ -290,7 +275,7 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
       }
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&hfull[hb]);  // release: this warp's reductions are visible to the folds
+        mbar_arrive(&hfull[hb]);  // release: this warp's reductions are visible to the fold warps
         if (u + S < nunits) {     // refill my slot (all its keys are in registers already)
           const int bn = p.b_begin + col_cta + (u + S) * ncol;
           mbar_arrive_expect_tx(&wfull[slot], wbytes * HALVES);
@@ -301,79 +286,109 @@ __global__ void __launch_bounds__(kScatterThreads, 1) scatter_kernel(const Scatt
         }
       }
     }
-    // fold my slice of unit f = u-1
-    const int f = u - 1;
-    if (f >= 0) {
+  } else {
+    // ============================= fold warps =============================
+    __syncthreads();
+    const int fw = warp - nwarps;  // fold warp index (kFoldWarps = 4: 2 warp bits)
+    // logical bin j = (fw*32 + lane) * 2^lb + e; lane bits start at lb, fold-warp bits at lb + 5
+    int lb = p.k - 5 - 2;
+    if (lb < 0) lb = 0;
+    const int fbase = (fw * 32 + lane) << lb;
+    const bool active = fbase < nbk;
+    int32_t prev[MAXNH];
+#pragma unroll
+    for (int i = 0; i < MAXNH; ++i) prev[i] = 0;
+    for (int f = 0; f < nunits; ++f) {
       const int fb = f % NH;
       const int32_t* H = hist + fb * nbk;
       mbar_wait(&hfull[fb], (uint32_t)((f / NH) & 1));
-      int32_t x[16];
+      // my bins: 2^lb <= 128 logical bins, same swizzle constant per 32-bin group
+      int32_t a[8];  // local-bit partials, lb <= 7
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = 0;
-      if (fold_active) {
-        const uint32_t c = ((uint32_t)fbase >> 5) & 31u;  // same for all my bins (<= 16, aligned)
+      for (int i = 0; i < 8; ++i) a[i] = 0;
+      int32_t X = 0;
+      if (active) {
+        const int4* H4 = reinterpret_cast<const int4*>(H);
         if (lb >= 2) {
-          const int4* H4 = reinterpret_cast<const int4*>(H);
+          const int n4 = 1 << (lb - 2);
+          for (int c4 = 0; c4 < n4; c4 += 4) {  // 4 int4 (16 bins) at a time
+            int4 z[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (i < (1 << (lb - 2))) {
-              const int4 z = unswizzle4(H4[((fbase >> 2) + i) ^ (int)(c >> 2)], c);
-              x[4 * i] = z.x; x[4 * i + 1] = z.y; x[4 * i + 2] = z.z; x[4 * i + 3] = z.w;
+            for (int i = 0; i < 4; ++i) {
+              const int j4 = (fbase >> 2) + c4 + i;  // logical int4 index
+              const uint32_t c = ((uint32_t)j4 >> 3) & 31u;
+              z[i] = (c4 + i < n4) ? unswizzle4(H4[j4 ^ (int)(c >> 2)], c) : make_int4(0, 0, 0, 0);
             }
+            int32_t x[16] = {z[0].x, z[0].y, z[0].z, z[0].w, z[1].x, z[1].y, z[1].z, z[1].w,
+                             z[2].x, z[2].y, z[2].z, z[2].w, z[3].x, z[3].y, z[3].z, z[3].w};
+            int32_t tot = 0;
+            if (FOLDPP) {  // pairwise compaction over the 4 bits inside the 16-bin chunk
+#pragma unroll
+              for (int L = 0; L < 4; ++L) {
+                const int cnt = 8 >> L;
+                int32_t odd = 0;
+#pragma unroll
+                for (int tt = 0; tt < 8; ++tt)
+                  if (tt < cnt) {
+                    odd += x[2 * tt + 1];
+                    x[tt] = x[2 * tt] + x[2 * tt + 1];
+                  }
+                a[L] += odd;
+              }
+              tot = x[0];
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+#pragma unroll
+                for (int L = 0; L < 4; ++L) a[L] += ((e >> L) & 1) ? x[e] : 0;
+                tot += x[e];
+              }
+            }
+            // chunk bits 4.. (chunk index c4/4) are local bits too
+            const int ci = c4 >> 2;
+#pragma unroll
+            for (int L = 4; L < 8; ++L) a[L] += ((ci >> (L - 4)) & 1) ? tot : 0;
+            X += tot;
+          }
         } else {
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
-            if (e < (1 << lb)) x[e] = H[key_swizzle((uint32_t)(fbase + e))];
+          for (int e = 0; e < 4; ++e)
+            if (e < (1 << lb)) {
+              const int32_t x = H[key_swizzle((uint32_t)(fbase + e))];
+              if (lb >= 1 && (e & 1)) a[0] += x;
+              X += x;
+            }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&hfree[fb]);  // release: my reads of the buffer are complete
-      int32_t a[16];
+      // slot i: 0-7 local bits (< lb), 8-12 lane bits, 13-14 fold-warp bits; lane i keeps slot i
+      int32_t r = 0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) a[i] = 0;
-      int32_t X = 0;
-      if (FOLDPP) {
-#pragma unroll
-        for (int L = 0; L < 4; ++L) {
-          if (L < lb) {
-            const int cnt = 8 >> L;
-            int32_t odd = 0;
-#pragma unroll
-            for (int tt = 0; tt < 8; ++tt)
-              if (tt < cnt) {
-                odd += x[2 * tt + 1];
-                x[tt] = x[2 * tt] + x[2 * tt + 1];
-              }
-            a[L] = odd;
-          }
+      for (int i = 0; i < 8; ++i)
+        if (i < lb) {
+          const int32_t tv = __reduce_add_sync(0xffffffffu, a[i]);
+          if (lane == i) r = tv;
         }
-        X = x[0];
-      } else {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-#pragma unroll
-          for (int L = 0; L < 4; ++L) a[L] += ((e >> L) & 1) ? x[e] : 0;
-          X += x[e];
-        }
+      for (int bit = 0; bit < 5; ++bit) {
+        const int32_t tv = __reduce_add_sync(0xffffffffu, ((lane >> bit) & 1) ? X : 0);
+        if (lane == 8 + bit) r = tv;
       }
-      // slots 0-3: local bits (< lb); 4-8: lane bits; 9-13: warp bits (uniform per warp)
-#pragma unroll
-      for (int bit = 0; bit < 5; ++bit) a[4 + bit] = ((lane >> bit) & 1) ? X : 0;
-#pragma unroll
-      for (int bit = 0; bit < 5; ++bit) a[9 + bit] = ((warp >> bit) & 1) ? X : 0;
-      const int32_t r = reduce_scatter16(a, lane);  // lanes 2i, 2i+1: slot i summed over the warp
+      const int32_t W = __reduce_add_sync(0xffffffffu, X);
+      if (lane == 13) r = (fw & 1) ? W : 0;
+      if (lane == 14) r = (fw & 2) ? W : 0;
       int32_t pv = 0;
 #pragma unroll
       for (int i = 0; i < MAXNH; ++i)
         if (i == fb) { pv = prev[i]; prev[i] = r; }
-      const int i = lane >> 1;
       int sh = -1;
-      if (i < 4) sh = i < lb ? i : -1;
-      else if (i < 9) sh = lb + (i - 4);
-      else if (i < 14) sh = (i - 9) < wbits ? lb + 5 + (i - 9) : -1;
+      if (lane < 8) sh = lane < lb ? lane : -1;
+      else if (lane < 13) sh = lb + (lane - 8);
+      else if (lane < 15) sh = lb + 5 + (lane - 13);
       const int b = p.b_begin + col_cta + f * ncol;
       const int w = block_width(p.cols, p.k, b);
-      if (!(lane & 1) && sh >= 0 && sh < w && r != pv) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)(r - pv));
+      if (sh >= 0 && sh < w && r != pv) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)(r - pv));
     }
   }
 }
@@ -669,7 +684,7 @@ rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int t
   if (st != RSR_OK) return st;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads);
+  cfg.blockDim = dim3(threads + 32 * kFoldWarps);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -700,13 +715,14 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
   int threads = 32;
   while (threads < kScatterThreads && (int64_t)threads * R < d.rows) threads *= 2;
   p.rows_per_cta = threads * R;
+  p.scatter_warps = threads / 32;
   p.n_splits = (int)((d.rows + p.rows_per_cta - 1) / p.rows_per_cta);
   p.atomic_out = p.n_splits > 1;
   const size_t slot_bytes = (size_t)d.halves * p.rows_per_cta * 2;
   const size_t max_smem = device_max_smem_optin();
   auto need = [&](int st, int nh) {
     return ((sizeof(int32_t) * ((((size_t)1 << d.k) * nh + 15) & ~(size_t)15) + 127) & ~(size_t)127) +
-           st * slot_bytes + 8 * ((threads / 32) * st + 2 * nh) + 64;
+           st * slot_bytes + 8 * ((threads / 32) * st + 2 * nh) + 64;  // + fold warps: no smem
   };
   // prefer >= 3 ring stages, then a third histogram buffer, then a 4th stage
   int stages = 0, nhist = 0;
@@ -716,12 +732,12 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
   if (!stages) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: index slice does not fit in shared memory");
   if (stages == 3 && nhist == 3 && need(4, 3) <= max_smem) stages = 4;
   if (const char* e = getenv("RSR_B200_STAGES")) stages = atoi(e);  // diagnostics
-  if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::min(6, std::max(2, atoi(e)));
+  if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::min(4, std::max(2, atoi(e)));
   p.stages = stages;
   p.nhist = nhist;
   const size_t smem = need(stages, nhist);
   // small CTAs (few rows) share an SM
-  const int per_sm = std::max<int>(1, (int)std::min<size_t>(2048 / threads, (228u << 10) / (smem + 1024)));
+  const int per_sm = std::max<int>(1, (int)std::min<size_t>(2048 / (threads + 32 * kFoldWarps), (228u << 10) / (smem + 1024)));
   const int nblk = b1 - b0;
   const int sms = device_sm_count();
   const int ncol = std::max(1, std::min(nblk, sms * per_sm / std::max(1, p.n_splits)));

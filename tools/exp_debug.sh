@@ -1,3 +1,3 @@
-python tools/prof_multiply.py --iters 3
-for dt in float32 int32 float64; do python tools/prof_multiply.py --iters 3 --form gather --dtype $dt; done
-python tools/prof_multiply.py --iters 3 --form gather --dtype float32 --variant rsr
+timeout 60 python tools/prof_multiply.py --iters 3
+timeout 60 python tools/prof_multiply.py --iters 3 --variant rsr
+for c in llama4096 llama14336x4096; do timeout 60 python tools/prof_multiply.py --iters 3 --config $c; done
