@@ -83,6 +83,8 @@ struct ScatterParams {
   int rows_per_cta, n_splits, stages, atomic_out, nhist;
   int v_aligned;
   int scatter_warps;
+  int sched;          // keys stored in scheduled order (k <= 11): x in bits 13-15 of each group's first code
+  uint32_t lo_mask;   // mask of the first code word's low half (clears the x bits)
 };
 
 template <typename OutT>
@@ -199,6 +201,8 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   if (!is_fold) {
     // =========================== scatter warps ===========================
     const bool all_valid = wr0 + 256 * (NG - 1) + 8 * lane + 8 <= p.rows;
+    const bool warp_all_valid = wr0 + 256 * (NG - 1) + 256 <= p.rows;  // every lane of the warp
+    const bool warp_none = wr0 >= p.rows;                                // a padding warp
     const uint32_t hist_s = smem_u32(hist);
     const uint32_t ring_s = smem_u32(ring);
     int32_t vr[R];
@@ -246,27 +250,52 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 #pragma unroll
           for (int g = 0; g < NG; ++g) qn[g] = make_uint4(0, 0, 0, 0);
         }
-        if (all_valid) {
+        if (warp_none) {
+        } else if (warp_all_valid) {
 #pragma unroll
           for (int g = 0; g < NG; ++g) {
-            const uint32_t w4[4] = {q[g].x, q[g].y, q[g].z, q[g].w};
+            // scheduled key order (k <= 11): this lane processes its 8 rows in order e ^ x,
+            // x in bits 13-15 of the first code; permute the v registers to match (3 SEL stages)
+            const uint32_t x = p.sched ? (q[g].x >> 13) & 7u : 0u;
+            int32_t vp[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) vp[e] = vr[g * 8 + e];
+#pragma unroll
+            for (int st = 0; st < 3; ++st) {
+              const bool sw = (x >> st) & 1u;
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (!(e & (1 << st))) {
+                  const int32_t a = vp[e], c = vp[e | (1 << st)];
+                  vp[e] = sw ? c : a;
+                  vp[e | (1 << st)] = sw ? a : c;
+                }
+            }
+            const uint32_t w4[4] = {q[g].x & p.lo_mask, q[g].y, q[g].z, q[g].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
+              const int32_t a = vp[2 * e], c = vp[2 * e + 1];
               red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
               red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
             }
           }
-        } else {  // rows past the end of the matrix were never copied: skip them
+        } else {  // the warp holding the end of the rows: rows past it were never copied
 #pragma unroll
           for (int g = 0; g < NG; ++g) {
             const int64_t row = wr0 + 256 * g + 8 * lane;
-            const uint32_t w4[4] = {q[g].x, q[g].y, q[g].z, q[g].w};
+            const uint32_t x = p.sched ? (q[g].x >> 13) & 7u : 0u;
+            const uint32_t w4[4] = {q[g].x & p.lo_mask, q[g].y, q[g].z, q[g].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const int32_t a = vr[g * 8 + 2 * e], c = vr[g * 8 + 2 * e + 1];
-              if (row + 2 * e < p.rows) red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
-              if (row + 2 * e + 1 < p.rows) red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
+              const int s0 = (2 * e) ^ (int)x, s1 = (2 * e + 1) ^ (int)x;  // source rows in the group
+              int32_t a = 0, c = 0;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (i == s0) a = vr[g * 8 + i];
+                if (i == s1) c = vr[g * 8 + i];
+              }
+              if (row + s0 < p.rows) red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
+              if (row + s1 < p.rows) red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
             }
           }
         }
@@ -716,6 +745,8 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
   while (threads < kScatterThreads && (int64_t)threads * R < d.rows) threads *= 2;
   p.rows_per_cta = threads * R;
   p.scatter_warps = threads / 32;
+  p.sched = d.k <= 11;
+  p.lo_mask = p.sched ? 0xffff1fffu : 0xffffffffu;
   p.n_splits = (int)((d.rows + p.rows_per_cta - 1) / p.rows_per_cta);
   p.atomic_out = p.n_splits > 1;
   const size_t slot_bytes = (size_t)d.halves * p.rows_per_cta * 2;

@@ -163,6 +163,107 @@ rsr_status launch_sort(const rsr_index_desc& d, void* workspace, size_t ws_bytes
   return cuda_check(cudaGetLastError(), "sort_blocks_kernel launch");
 }
 
+// ---------------------------------------------------------------------------------------
+// Key-order scheduling for the scatter kernel's shared-memory reductions (k <= 11).
+// The scatter kernel issues one reduction instruction per (8-row group, position e) with
+// lane l handling row 256c + 8l + e of 256-row chunk c; its cost is the number of bank
+// wavefronts = the largest number of lanes that hit one bank.  Inside its group a lane may
+// process its 8 rows in any order e -> e ^ x_l: one warp per (block, chunk) picks x_l (3
+// bits, shared by both halves) by greedy coordinate descent on the number of colliding
+// lane pairs per (half, e, bank), stores the codes permuted, and records x_l in bits 13-15
+// of the lane's first code (free: codes are <= 8188 for k <= 11).  Simulated on uniform
+// ternary keys: -22% wavefronts.  Results are unchanged (integer sums are order-free).
+constexpr int kSchedWarps = 8;
+
+__global__ void __launch_bounds__(kSchedWarps * 32) schedule_keys_kernel(rsr_index_desc d, int sweeps) {
+  __shared__ int cnt_all[kSchedWarps][2][8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t nchunks = d.row_stride / 256;  // only whole 256-row chunks are scheduled
+  const int64_t task = (int64_t)blockIdx.x * kSchedWarps + wib;
+  if (task >= (int64_t)d.nblocks * nchunks) return;
+  const int b = (int)(task / nchunks);
+  const int64_t c = task % nchunks;
+  int (*cnt)[8][32] = cnt_all[wib];
+  uint16_t* code[2] = {nullptr, nullptr};
+  uint32_t kc[2][8] = {};
+  for (int h = 0; h < d.halves; ++h) {
+    code[h] = d.half[h].bucket + (int64_t)b * d.row_stride + c * 256 + 8 * lane;
+    const uint4 q = *reinterpret_cast<const uint4*>(code[h]);
+    const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      kc[h][2 * e] = w4[e] & 0xffffu;
+      kc[h][2 * e + 1] = w4[e] >> 16;
+    }
+  }
+  for (int i = lane; i < 2 * 8 * 32; i += 32) (&cnt[0][0][0])[i] = 0;
+  __syncwarp();
+  int x = 0;
+  for (int h = 0; h < d.halves; ++h)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) atomicAdd(&cnt[h][e][(kc[h][e] >> 2) & 31], 1);
+  __syncwarp();
+  for (int sweep = 0; sweep < sweeps; ++sweep) {
+    for (int l = 0; l < 32; ++l) {
+      // lane l's banks, broadcast
+      uint32_t bk[2][8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) bk[h][e] = __shfl_sync(0xffffffffu, (kc[h][e] >> 2) & 31, l);
+      const int xl = __shfl_sync(0xffffffffu, x, l);
+      if (lane == l)
+        for (int h = 0; h < d.halves; ++h)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) cnt[h][e][bk[h][e ^ xl]] -= 1;
+      __syncwarp();
+      // lane cand (< 8) evaluates candidate order e -> e ^ cand
+      int cost = 0x7fffffff;
+      if (lane < 8) {
+        cost = 0;
+        for (int h = 0; h < d.halves; ++h)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) cost += cnt[h][e][bk[h][e ^ lane]];
+        cost = cost * 8 + lane;  // ties -> smallest candidate
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cost = min(cost, __shfl_xor_sync(0xffffffffu, cost, o));
+      const int nx = cost & 7;
+      if (lane == l) {
+        x = nx;
+        for (int h = 0; h < d.halves; ++h)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) cnt[h][e][bk[h][e ^ nx]] += 1;
+      }
+      __syncwarp();
+    }
+  }
+  // write the codes in the scheduled order, x in bits 13-15 of position 0
+  for (int h = 0; h < d.halves; ++h) {
+    uint32_t o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int src = 0; src < 8; ++src)
+        if (src == (e ^ x)) v = kc[h][src];
+      o[e] = v;
+    }
+    o[0] |= (uint32_t)x << 13;
+    *reinterpret_cast<uint4*>(code[h]) =
+        make_uint4(o[0] | (o[1] << 16), o[2] | (o[3] << 16), o[4] | (o[5] << 16), o[6] | (o[7] << 16));
+  }
+}
+
+rsr_status launch_schedule(const rsr_index_desc& d, cudaStream_t s) {
+  if (d.k > 11) return RSR_OK;  // no spare code bits: keys stay in row order
+  const int64_t tasks = (int64_t)d.nblocks * (d.row_stride / 256);
+  if (tasks == 0) return RSR_OK;
+  const unsigned grid = (unsigned)((tasks + kSchedWarps - 1) / kSchedWarps);
+  schedule_keys_kernel<<<grid, kSchedWarps * 32, 0, s>>>(d, 2);
+  return cuda_check(cudaGetLastError(), "schedule_keys_kernel launch");
+}
+
 rsr_status clear_index(const rsr_index_desc& d, cudaStream_t s) {
   for (int h = 0; h < d.halves; ++h) {
     size_t nb = (size_t)d.nblocks * d.row_stride;
@@ -204,7 +305,8 @@ rsr_status preprocess_ternary(const int8_t* A, int64_t lda, const rsr_index_desc
   keys_ternary_kernel<<<grid, kKeyThreads, 0, s>>>(A, lda, d->rows, d->cols, d->k, bt, d->row_stride,
                                                    d->half[0].bucket, d->half[1].bucket, bad);
   if ((st = cuda_check(cudaGetLastError(), "keys_ternary_kernel launch")) != RSR_OK) return st;
-  return launch_sort(*d, ws, ws_bytes, s);
+  if ((st = launch_sort(*d, ws, ws_bytes, s)) != RSR_OK) return st;
+  return launch_schedule(*d, s);
 }
 
 rsr_status preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_desc* d, void* ws, size_t ws_bytes,
@@ -218,7 +320,8 @@ rsr_status preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_d
   keys_binary_kernel<<<grid, 256, 0, s>>>(bits, ldb, d->rows, d->cols, d->k, d->nblocks, d->row_stride,
                                           d->half[0].bucket);
   if ((st = cuda_check(cudaGetLastError(), "keys_binary_kernel launch")) != RSR_OK) return st;
-  return launch_sort(*d, ws, ws_bytes, s);
+  if ((st = launch_sort(*d, ws, ws_bytes, s)) != RSR_OK) return st;
+  return launch_schedule(*d, s);
 }
 
 }  // namespace rsr
