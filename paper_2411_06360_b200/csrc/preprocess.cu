@@ -12,6 +12,8 @@
 // warp-private shared-memory counter array, scans it into `seg`, and then walks
 // the rows in ascending order 32 at a time, ranking equal keys with
 // __match_any_sync so the scatter into `perm` is stable by construction.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rsr {
@@ -257,6 +259,8 @@ __global__ void __launch_bounds__(kSchedWarps * 32) schedule_keys_kernel(rsr_ind
 
 rsr_status launch_schedule(const rsr_index_desc& d, cudaStream_t s) {
   if (d.k > 11) return RSR_OK;  // no spare code bits: keys stay in row order
+  if (const char* e = getenv("RSR_B200_NOSCHED"))
+    if (e[0] == '1') return RSR_OK;  // diagnostics
   const int64_t tasks = (int64_t)d.nblocks * (d.row_stride / 256);
   if (tasks == 0) return RSR_OK;
   const unsigned grid = (unsigned)((tasks + kSchedWarps - 1) / kSchedWarps);

@@ -1,3 +1,4 @@
-timeout 60 python tools/prof_multiply.py --iters 3
-timeout 60 python tools/prof_multiply.py --iters 3 --variant rsr
-for c in llama4096 llama14336x4096; do timeout 60 python tools/prof_multiply.py --iters 3 --config $c; done
+for c in llama4096x14336 ternary16384 llama4096; do
+timeout 60 python tools/prof_multiply.py --iters 3 --config $c
+RSR_B200_NOSCHED=1 timeout 60 python tools/prof_multiply.py --iters 3 --config $c | sed 's/^/nosched /'
+done
