@@ -25,4 +25,10 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean
+# diagnostic build with per-unit timestamps (tools/trace_scatter.py); not used by the product
+TRACE_LIB := paper_2411_06360_b200/lib/trace/librsr_b200_trace.so
+trace: $(SRC) $(HDR)
+	@mkdir -p $(dir $(TRACE_LIB))
+	$(NVCC) $(NVFLAGS) -DRSR_TRACE -shared -o $(TRACE_LIB) $(SRC) -lcudart
+
+.PHONY: all oracle clean trace

@@ -74,6 +74,26 @@ __device__ __forceinline__ T reduce_scatter16(T (&a)[16], int lane) {
 // SCATTER kernel (int32)
 // =====================================================================================
 
+#ifdef RSR_TRACE
+// Diagnostic build only (`make trace`, tools/trace_scatter.py): per-unit globaltimer stamps.
+__device__ unsigned long long g_trace[148 * 512];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot) do { if (lane == 0 && blockIdx.x < 148) g_trace[blockIdx.x * 512 + (slot)] = gtimer(); } while (0)
+}  // namespace
+}  // namespace rsr
+extern "C" int rsr_debug_trace_copy(unsigned long long* host, size_t n) {
+  return (int)cudaMemcpyFromSymbol(host, rsr::g_trace, n * sizeof(unsigned long long));
+}
+namespace rsr {
+namespace {
+#else
+#define TRACE(slot) do { } while (0)
+#endif
+
 struct ScatterParams {
   const uint16_t* key[2];
   const int32_t* v;
@@ -160,6 +180,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   const uint16_t* key1 = p.key[1];
   OutT* out = reinterpret_cast<OutT*>(p.out);
   const bool is_fold = warp >= nwarps;
+  if (warp == 0) TRACE(0);
 
   // ---- prologue (index only: may overlap the previous kernel under PDL) ----
   uint16_t* ring = ring_all + (size_t)(is_fold ? 0 : warp) * S * HALVES * WROWS;  // my [S][HALVES][WROWS]
@@ -221,6 +242,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       }
     }
     __syncthreads();
+    if (warp == 0) TRACE(1);
     auto load_keys = [&](int slot, int h, uint4 (&q)[NG]) {
       const uint32_t base = ring_s + (uint32_t)(((slot * HALVES + h) * WROWS + 8 * lane) * 2);
 #pragma unroll
@@ -236,7 +258,9 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       const int slot = u % S;
       const int hb = u % NH;
       const uint32_t Hs = hist_s + (uint32_t)(hb * nbk) * 4u;
+      if (warp == 0 && u < 40) TRACE(8 + u * 8 + 0);
       if (u >= NH) mbar_wait(&hfree[hb], (uint32_t)(((u / NH) - 1) & 1));
+      if (warp == 0 && u < 40) TRACE(8 + u * 8 + 1);
 #pragma unroll
       for (int h = 0; h < HALVES; ++h) {
         uint4 qn[NG];  // next half-block's keys, loaded before this half's reductions
@@ -303,8 +327,10 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         for (int g = 0; g < NG; ++g) q[g] = qn[g];
       }
       __syncwarp();
+      if (warp == 0 && u < 40) TRACE(8 + u * 8 + 2);
       if (lane == 0) {
         mbar_arrive(&hfull[hb]);  // release: this warp's reductions are visible to the fold warps
+        if (warp == 0 && u < 40) TRACE(8 + u * 8 + 7);
         if (u + S < nunits) {     // refill my slot (all its keys are in registers already)
           const int bn = p.b_begin + col_cta + (u + S) * ncol;
           mbar_arrive_expect_tx(&wfull[slot], wbytes * HALVES);
@@ -313,6 +339,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
               tma_load_1d(ring + ((size_t)slot * HALVES + h) * WROWS,
                           (h ? key1 : key0) + (int64_t)bn * p.row_stride + wr0, wbytes, &wfull[slot], policy);
         }
+        if (warp == 0 && u < 40) TRACE(300 + u);
       }
     }
   } else {
@@ -330,7 +357,9 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     for (int f = 0; f < nunits; ++f) {
       const int fb = f % NH;
       const int32_t* H = hist + fb * nbk;
+      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 3);
       mbar_wait(&hfull[fb], (uint32_t)((f / NH) & 1));
+      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 4);
       // my bins: 2^lb <= 128 logical bins, same swizzle constant per 32-bin group
       int32_t a[8];  // local-bit partials, lb <= 7
 #pragma unroll
@@ -390,6 +419,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         }
       }
       __syncwarp();
+      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 5);
       if (lane == 0) mbar_arrive(&hfree[fb]);  // release: my reads of the buffer are complete
       // slot i: 0-7 local bits (< lb), 8-12 lane bits, 13-14 fold-warp bits; lane i keeps slot i
       int32_t r = 0;
@@ -418,8 +448,10 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       const int b = p.b_begin + col_cta + f * ncol;
       const int w = block_width(p.cols, p.k, b);
       if (sh >= 0 && sh < w && r != pv) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)(r - pv));
+      if (fw == 0 && f < 40) TRACE(400 + f);
     }
   }
+  if (warp == 0) TRACE(7);
 }
 
 // =====================================================================================
