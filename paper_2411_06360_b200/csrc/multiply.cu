@@ -469,7 +469,8 @@ struct GatherParams {
 };
 
 constexpr int kGatherWarps = 8;
-constexpr int kPermAhead = 4;  // perm windows in flight per warp (16-byte loads, registers)  // one CTA works on one column block at a time
+constexpr int kPermAhead = 4;  // perm windows in flight per warp (16-byte loads, registers)
+constexpr int kMaxWin = 64;    // windows per warp position range: rows <= 64 * 256 * ranges per half
 
 template <typename T>
 __device__ __forceinline__ T vload(const T* vs, const T* vg, uint32_t row, bool smem) {
@@ -479,13 +480,17 @@ __device__ __forceinline__ T vload(const T* vs, const T* vg, uint32_t row, bool 
 // One CTA per column block at a time (persistent over blocks).  The 8 warps split the block's
 // sorted positions: (half, part) = (warp / P, warp % P), P = 8 / halves contiguous position
 // ranges per half.  Per 256-position window a warp gathers v[perm[p]] from shared memory (8
-// positions per lane, perm prefetched one window ahead), forms window-local prefix sums with a
-// warp scan, and every bucket boundary j (position seg[j], seg staged in shared memory) adds
-// its prefix with the RSR++ telescoping coefficients bit_s(j-1) - bit_s(j) — the pairwise
-// compaction of Alg. 3 applied to prefix sums, ~2 adds per bucket — or, for variant "rsr",
-// forms the segment sum and adds it to every column whose bit is set.  The bucket open at a
-// range / window end contributes the remaining tail.  Linear, so the warps' partial column
-// sums are combined in a fixed order: deterministic, no float atomics.
+// positions per lane; perm streamed kPermAhead windows ahead with 16-byte loads) and forms
+// window-local prefix sums with a warp scan (stored transposed: conflict-free).  Every bucket
+// boundary j (position seg[j], seg staged in shared memory) contributes its prefix P with the
+// RSR++ telescoping coefficients bit_s(j-1) - bit_s(j) — the pairwise compaction of Alg. 3
+// applied to prefix sums: the lane adds P to its private slot B[ctz(j)], and at the range end
+// column s receives sum_{t>s} B[t] - B[s] (two adds per bucket overall).  For variant "rsr"
+// the boundary forms the segment sum u and adds it to every column whose bit is set (the dense
+// product).  The bucket open at a window end contributes the window total with its bit
+// pattern (one (bucket, total) record per window, expanded in parallel at the range end).
+// Everything is linear, so the warps' partial column sums are combined in a fixed order:
+// deterministic, no float atomics.
 template <typename T, bool FOLDPP>
 __global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -495,18 +500,24 @@ __global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherP
   T* pbuf_all = reinterpret_cast<T*>(segs + 2 * seg_words);                  // [8][256]
   T* pbuf = pbuf_all + warp * 256;
   T* part = pbuf_all + kGatherWarps * 256;                                   // [8][16]
-  T* vs = part + kGatherWarps * 16;
+  T* Bl_all = part + kGatherWarps * 16;                                      // [8][32 lanes][17] telescoping slots
+  T* Bl = Bl_all + (warp * 32 + lane) * 17;
+  T* etot_all = Bl_all + kGatherWarps * 32 * 17;                             // [8][kMaxWin] window-end totals
+  int* ebkt_all = reinterpret_cast<int*>(etot_all + kGatherWarps * kMaxWin); // [8][kMaxWin] window-end buckets
+  T* etot = etot_all + warp * kMaxWin;
+  int* ebkt = ebkt_all + warp * kMaxWin;
+  T* vs = reinterpret_cast<T*>(ebkt_all + kGatherWarps * kMaxWin);
   const T* vg = reinterpret_cast<const T*>(p.v);
   const bool vsm = p.v_in_smem != 0;
-  if (vsm) {
-    for (int64_t i = threadIdx.x; i < p.rows; i += blockDim.x) vs[i] = vg[i];
-  }
+  if (vsm)
+    for (int i = threadIdx.x; i < (int)p.rows; i += blockDim.x) vs[i] = vg[i];
   T* out = reinterpret_cast<T*>(p.out);
   const int P = kGatherWarps / p.halves;  // position ranges per half
   const int h = warp / P, part_i = warp % P;
-  const int64_t plen = ((p.rows + P - 1) / P + 255) / 256 * 256;  // window-aligned range length
-  const int64_t P0 = (int64_t)part_i * plen;
-  const int64_t P1 = std::min<int64_t>(p.rows, P0 + plen);
+  const int rows = (int)p.rows;
+  const int plen = ((rows + P - 1) / P + 255) / 256 * 256;  // window-aligned range length
+  const int P0 = part_i * plen;
+  const int P1 = min(rows, P0 + plen);
   const uint32_t* seg0 = p.seg[0];
   const uint32_t* seg1 = p.seg[1];
   const void* perm_g = h ? p.perm[1] : p.perm[0];
@@ -521,25 +532,27 @@ __global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherP
         const int hh = i / (nbk + 1), j = i % (nbk + 1);
         segs[hh * seg_words + j] = (hh ? seg1 : seg0)[(int64_t)b * p.seg_stride + j];
       }
+#pragma unroll
+    for (int i = 0; i < 17; ++i) Bl[i] = T(0);
     __syncthreads();
     const uint32_t* seg = p.seg_in_smem ? segs + h * seg_words : (h ? seg1 : seg0) + (int64_t)b * p.seg_stride;
-    T acc[kMaxK];
+    T acc[kMaxK];  // dense ("rsr") accumulation only
 #pragma unroll
     for (int s = 0; s < kMaxK; ++s) acc[s] = T(0);
+    int nwin = 0;
     if (P0 < P1) {
       // first boundary after P0: jcur = 1 + #{j in [1, nbk] : seg[j] <= P0}
       int lo = 1, hi = nbk + 1;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if ((int64_t)seg[mid] <= P0) lo = mid + 1; else hi = mid;
+        if ((int)seg[mid] <= P0) lo = mid + 1; else hi = mid;
       }
       int jcur = (P0 == 0) ? 1 : lo;
       T carry = T(0);
       const uint16_t* perm16 = reinterpret_cast<const uint16_t*>(perm_g) + (int64_t)b * p.row_stride;
       const uint32_t* perm32 = reinterpret_cast<const uint32_t*>(perm_g) + (int64_t)b * p.row_stride;
-      // perm stream: kPermAhead windows of 16-byte loads in flight (register ring)
-      auto load_perm = [&](int64_t w0, uint4 (&q)[2]) {
-        const int64_t pos0 = w0 + 8 * lane;
+      auto load_perm = [&](int w0, uint4 (&q)[2]) {
+        const int pos0 = w0 + 8 * lane;
         q[0] = q[1] = make_uint4(0, 0, 0, 0);
         if (pos0 < P1) {
           if (p.perm_bytes == 2) {
@@ -553,96 +566,108 @@ __global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherP
       uint4 ring[kPermAhead][2];
 #pragma unroll
       for (int i = 0; i < kPermAhead; ++i) load_perm(P0 + 256 * i, ring[i]);
-      int rslot = 0;
-      for (int64_t w0 = P0; w0 < P1; w0 += 256) {
-        const int E = (int)std::min<int64_t>(256, P1 - w0);
-        const int64_t pos0 = w0 + 8 * lane;
-        uint4 q0 = ring[0][0], q1 = ring[0][1];
+      for (int wb = P0; wb < P1; wb += 256 * kPermAhead) {
 #pragma unroll
-        for (int i = 1; i < kPermAhead; ++i)
-          if (i == rslot) { q0 = ring[i][0]; q1 = ring[i][1]; }
-        uint32_t rowsel[8];
-        if (p.perm_bytes == 2) {
-          rowsel[0] = q0.x & 0xffffu; rowsel[1] = q0.x >> 16; rowsel[2] = q0.y & 0xffffu; rowsel[3] = q0.y >> 16;
-          rowsel[4] = q0.z & 0xffffu; rowsel[5] = q0.z >> 16; rowsel[6] = q0.w & 0xffffu; rowsel[7] = q0.w >> 16;
-        } else {
-          rowsel[0] = q0.x; rowsel[1] = q0.y; rowsel[2] = q0.z; rowsel[3] = q0.w;
-          rowsel[4] = q1.x; rowsel[5] = q1.y; rowsel[6] = q1.z; rowsel[7] = q1.w;
-        }
-        T x[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = (pos0 + e < P1) ? vload(vs, vg, rowsel[e], vsm) : T(0);
-        {  // refill this ring slot with the window kPermAhead ahead
-          uint4 nq[2];
-          load_perm(w0 + 256 * kPermAhead, nq);
-#pragma unroll
-          for (int i = 0; i < kPermAhead; ++i)
-            if (i == rslot) { ring[i][0] = nq[0]; ring[i][1] = nq[1]; }
-          rslot = rslot + 1 == kPermAhead ? 0 : rslot + 1;
-        }
-#pragma unroll
-        for (int e = 1; e < 8; ++e) x[e] += x[e - 1];
-        const T incl = warp_inclusive_scan(x[7], lane);
-        const T base = incl - x[7];
-        const T total = __shfl_sync(0xffffffffu, incl, 31);
-        // transposed prefix buffer: position 8*lane + e lives at e*32 + lane (conflict-free stores)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) pbuf[e * 32 + lane] = base + x[e];
-        __syncwarp();
-        int last_in = -1;
-        T p_last = T(0);
-        while (true) {
-          const int jj = jcur + lane;
-          const int64_t sj = jj <= nbk ? (int64_t)seg[jj] : INT64_MAX;
-          const bool in = sj <= w0 + E;
-          const int cnt = __popc(__ballot_sync(0xffffffffu, in));
-          T Pv = T(0);
-          if (in) {
-            const int q = (int)(sj - w0) - 1;
-            Pv = q >= 0 ? pbuf[((q & 7) << 5) | (q >> 3)] : T(0);
-          }
-          if (FOLDPP) {
-            if (in) {
-              const int tz = __ffs(jj) - 1;  // boundary j closes bucket j-1 and opens bucket j
-#pragma unroll
-              for (int s = 0; s < kMaxK; ++s) acc[s] += (s < tz) ? sgn * Pv : ((s == tz) ? -sgn * Pv : T(0));
+        for (int ri = 0; ri < kPermAhead; ++ri) {  // static ring slots: no register shuffling
+          const int w0 = wb + 256 * ri;
+          if (w0 < P1) {
+            const int E = min(256, P1 - w0);
+            const int pos0 = w0 + 8 * lane;
+            uint32_t rowsel[8];
+            if (p.perm_bytes == 2) {
+              const uint4 q0 = ring[ri][0];
+              rowsel[0] = q0.x & 0xffffu; rowsel[1] = q0.x >> 16; rowsel[2] = q0.y & 0xffffu; rowsel[3] = q0.y >> 16;
+              rowsel[4] = q0.z & 0xffffu; rowsel[5] = q0.z >> 16; rowsel[6] = q0.w & 0xffffu; rowsel[7] = q0.w >> 16;
+            } else {
+              const uint4 q0 = ring[ri][0], q1 = ring[ri][1];
+              rowsel[0] = q0.x; rowsel[1] = q0.y; rowsel[2] = q0.z; rowsel[3] = q0.w;
+              rowsel[4] = q1.x; rowsel[5] = q1.y; rowsel[6] = q1.z; rowsel[7] = q1.w;
             }
-          } else {
-            const T prevP = __shfl_up_sync(0xffffffffu, Pv, 1);
-            if (in) {
-              const T uj = (lane == 0) ? carry + Pv : Pv - prevP;
-              const int j = jj - 1;
+            T x[8];
 #pragma unroll
-              for (int s = 0; s < kMaxK; ++s) acc[s] += ((j >> s) & 1) ? sgn * uj : T(0);
-            }
-            if (cnt > 0) {
-              p_last = __shfl_sync(0xffffffffu, Pv, cnt - 1);
-              carry = T(0);
-              last_in = cnt - 1;
-            }
-          }
-          jcur += cnt;
-          if (cnt < 32) break;
-          if (!FOLDPP) carry = T(0) - p_last;
-        }
-        if (FOLDPP) {
-          const int g = jcur - 1;  // bucket open at the window end: its tail is the window total
-          if (lane == 0) {
+            for (int e = 0; e < 8; ++e) x[e] = (pos0 + e < P1) ? vload(vs, vg, rowsel[e], vsm) : T(0);
+            load_perm(w0 + 256 * kPermAhead, ring[ri]);  // refill this slot
 #pragma unroll
-            for (int s = 0; s < kMaxK; ++s) acc[s] += ((g >> s) & 1) ? sgn * total : T(0);
+            for (int e = 1; e < 8; ++e) x[e] += x[e - 1];
+            const T incl = warp_inclusive_scan(x[7], lane);
+            const T base = incl - x[7];
+            const T total = __shfl_sync(0xffffffffu, incl, 31);
+            // transposed prefix buffer: position 8*lane + e lives at e*32 + lane (conflict-free)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pbuf[e * 32 + lane] = base + x[e];
+            __syncwarp();
+            int last_in = -1;
+            T p_last = T(0);
+            while (true) {
+              const int jj = jcur + lane;
+              const int sj = jj <= nbk ? (int)seg[jj] : 0x7fffffff;
+              const bool in = sj <= w0 + E;
+              const int cnt = __popc(__ballot_sync(0xffffffffu, in));
+              T Pv = T(0);
+              if (in) {
+                const int q = sj - w0 - 1;
+                Pv = q >= 0 ? pbuf[((q & 7) << 5) | (q >> 3)] : T(0);
+              }
+              if (FOLDPP) {
+                if (in) {  // boundary j closes bucket j-1, opens bucket j: +P below ctz(j), -P at ctz(j)
+                  const int tz = __ffs(jj) - 1;
+                  Bl[tz] += sgn * Pv;
+                }
+              } else {
+                const T prevP = __shfl_up_sync(0xffffffffu, Pv, 1);
+                if (in) {
+                  const T uj = (lane == 0) ? carry + Pv : Pv - prevP;
+                  const int j = jj - 1;
+#pragma unroll
+                  for (int s = 0; s < kMaxK; ++s) acc[s] += ((j >> s) & 1) ? sgn * uj : T(0);
+                }
+                if (cnt > 0) {
+                  p_last = __shfl_sync(0xffffffffu, Pv, cnt - 1);
+                  carry = T(0);
+                  last_in = cnt - 1;
+                }
+              }
+              jcur += cnt;
+              if (cnt < 32) break;
+              if (!FOLDPP) carry = T(0) - p_last;
+            }
+            if (FOLDPP) {  // bucket open at the window end: its tail is the window total
+              if (lane == 0) {
+                ebkt[nwin] = jcur - 1;
+                etot[nwin] = sgn * total;
+              }
+              ++nwin;
+            } else {
+              carry = (last_in >= 0) ? total - p_last : carry + total;
+            }
+            __syncwarp();
           }
-        } else {
-          carry = (last_in >= 0) ? total - p_last : carry + total;
         }
-        __syncwarp();
       }
       if (!FOLDPP) {
-        // the bucket still open at the range end gets the carried tail
-        const int g = jcur - 1;
-        if (lane == 0 && P1 < p.rows) {
+        const int g = jcur - 1;  // the bucket still open at the range end gets the carried tail
+        if (lane == 0 && P1 < rows) {
 #pragma unroll
           for (int s = 0; s < kMaxK; ++s) acc[s] += ((g >> s) & 1) ? sgn * carry : T(0);
         }
+      }
+    }
+    if (FOLDPP) {
+      __syncwarp();
+      // telescoping slots -> columns: acc[s] = sum_{t > s} B[t] - B[s]
+      T suffix = T(0);
+#pragma unroll
+      for (int s = kMaxK; s >= 0; --s) {
+        const T bs = Bl[s];
+        if (s < kMaxK) acc[s] = suffix - bs;
+        suffix += bs;
+      }
+      // window-end records, one per lane
+      for (int i = lane; i < nwin; i += 32) {
+        const int g = ebkt[i];
+        const T tt = etot[i];
+#pragma unroll
+        for (int s = 0; s < kMaxK; ++s) acc[s] += ((g >> s) & 1) ? tt : T(0);
       }
     }
     const T r = reduce_scatter16(acc, lane);  // lanes 2s, 2s+1: warp total of column shift s
@@ -839,7 +864,10 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
   p.b_end = b1;
   p.perm_bytes = d.perm_bytes;
   const size_t max_smem = device_max_smem_optin();
-  const size_t pbuf_bytes = sizeof(T) * (kGatherWarps * 256 + kGatherWarps * 16);
+  const size_t pbuf_bytes = sizeof(T) * (kGatherWarps * 256 + kGatherWarps * 16 + kGatherWarps * 32 * 17 +
+                                         kGatherWarps * kMaxWin) + sizeof(int) * kGatherWarps * kMaxWin;
+  if (d.rows > (int64_t)kMaxWin * 256 * (kGatherWarps / d.halves))
+    return fail(RSR_ERR_UNSUPPORTED, "gather multiply supports at most 65536 (ternary) / 131072 (binary) rows");
   p.seg_in_smem = sizeof(uint32_t) * 2 * (size_t)((d.seg_stride + 3) & ~3) + pbuf_bytes <= (96u << 10);
   const size_t seg_words = p.seg_in_smem ? (size_t)((d.seg_stride + 3) & ~3) : 0;
   const size_t fixed = sizeof(uint32_t) * 2 * seg_words + pbuf_bytes;
