@@ -149,9 +149,25 @@ __device__ __forceinline__ int4 unswizzle4(int4 q, uint32_t c) {
 //  * Histogram buffers are never zeroed: block u adds into buffer u % NH on top of block
 //    u - NH; each fold lane keeps its previous fold of the buffer and adds the difference
 //    (exact modulo 2^32).
-template <int R, bool FOLDPP, bool TERNARY, typename OutT>
+// Quantization exponent for the FX path: the CTA max |v| (float bits in fxmax[0..n)) maps to
+// just below 2^30, so |v_q| < 2^30 and every limb sum over <= 16384 rows fits in int32.
+__device__ __forceinline__ int fx_exponent(const uint32_t* fxmax, int n) {
+  uint32_t m = 0;
+  for (int i = 0; i < n; ++i) m = max(m, fxmax[i]);
+  if (m == 0) return 0;
+  const float mf = __uint_as_float(m);
+  return 29 - ilogbf(mf);  // mf < 2^(ilogb+1) -> |v| * 2^e < 2^30
+}
+
+// FX (fp32 activations): v is quantized once per launch to 31-bit fixed point with a per-CTA
+// power-of-two scale (2^-31 of max|v|, far below fp32 rounding) and accumulated EXACTLY as two
+// 16-bit limbs in two int32 histograms (integer atomics are native; fp32 shared atomics are a
+// CAS loop on sm_100).  Deterministic, and more accurate than fp32 summation.  Single row
+// split only (one scale per output column).
+template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX>
 __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
   static_assert(R % 8 == 0 && R * kScatterThreads <= 16384, "rows per CTA");
+  constexpr int LIMBS = FX ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int HALVES = TERNARY ? 2 : 1;
   constexpr int NG = R / 8;      // 8-row groups per lane
@@ -163,12 +179,14 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   const int nbk = 1 << p.k;
   const int S = p.stages;
   const int NH = p.nhist;
-  const int hist_words = (NH * nbk + 15) & ~15;
-  int32_t* hist = reinterpret_cast<int32_t*>(smem);  // [NH][nbk]
+  const int hist_words = (NH * LIMBS * nbk + 15) & ~15;
+  int32_t* hist = reinterpret_cast<int32_t*>(smem);  // [NH][LIMBS][nbk]
   uint16_t* ring_all = reinterpret_cast<uint16_t*>(smem + ((sizeof(int32_t) * hist_words + 127) & ~(size_t)127));
   uint64_t* wfull_all = reinterpret_cast<uint64_t*>(ring_all + (size_t)nwarps * S * HALVES * WROWS);
   uint64_t* hfull = wfull_all + nwarps * S;
   uint64_t* hfree = hfull + NH;
+  uint32_t* fxmax = reinterpret_cast<uint32_t*>(hfree + NH);                   // [16] per-warp max |v| bits
+  long long* fxpart = reinterpret_cast<long long*>(fxmax + 16);                // [2][kFoldWarps][16]
 
   const int split = blockIdx.x % p.n_splits;
   const int col_cta = blockIdx.x / p.n_splits;
@@ -241,7 +259,19 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;
       }
     }
+    if constexpr (FX) {  // CTA max |v| -> quantization scale
+      uint32_t m = 0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) m = max(m, (uint32_t)vr[i] & 0x7fffffffu);
+      m = __reduce_max_sync(0xffffffffu, m);
+      if (lane == 0) fxmax[warp] = m;
+    }
     __syncthreads();
+    if constexpr (FX) {
+      const int e = fx_exponent(fxmax, nwarps);
+#pragma unroll
+      for (int i = 0; i < R; ++i) vr[i] = __float2int_rn(ldexpf(__int_as_float(vr[i]), e));
+    }
     if (warp == 0) TRACE(1);
     auto load_keys = [&](int slot, int h, uint4 (&q)[NG]) {
       const uint32_t base = ring_s + (uint32_t)(((slot * HALVES + h) * WROWS + 8 * lane) * 2);
@@ -257,7 +287,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       if (u + 1 == nunits) grid_launch_dependents();  // the next grid may start its prologue on freed SMs
       const int slot = u % S;
       const int hb = u % NH;
-      const uint32_t Hs = hist_s + (uint32_t)(hb * nbk) * 4u;
+      const uint32_t Hs = hist_s + (uint32_t)(hb * LIMBS * nbk) * 4u;
       if (warp == 0 && u < 40) TRACE(8 + u * 8 + 0);
       if (u >= NH) mbar_wait(&hfree[hb], (uint32_t)(((u / NH) - 1) & 1));
       if (warp == 0 && u < 40) TRACE(8 + u * 8 + 1);
@@ -299,8 +329,16 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int32_t a = vp[2 * e], c = vp[2 * e + 1];
-              red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
-              red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
+              if constexpr (FX) {
+                const uint32_t lo_off = (uint32_t)nbk * 4u;
+                red_add_shared(Hs + (w4[e] & 0xffffu), h ? -(a >> 16) : (a >> 16));
+                red_add_shared(Hs + lo_off + (w4[e] & 0xffffu), h ? -(a & 0xffff) : (a & 0xffff));
+                red_add_shared(Hs + (w4[e] >> 16), h ? -(c >> 16) : (c >> 16));
+                red_add_shared(Hs + lo_off + (w4[e] >> 16), h ? -(c & 0xffff) : (c & 0xffff));
+              } else {
+                red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
+                red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
+              }
             }
           }
         } else {  // the warp holding the end of the rows: rows past it were never copied
@@ -318,8 +356,20 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
                 if (i == s0) a = vr[g * 8 + i];
                 if (i == s1) c = vr[g * 8 + i];
               }
-              if (row + s0 < p.rows) red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
-              if (row + s1 < p.rows) red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
+              if constexpr (FX) {
+                const uint32_t lo_off = (uint32_t)nbk * 4u;
+                if (row + s0 < p.rows) {
+                  red_add_shared(Hs + (w4[e] & 0xffffu), h ? -(a >> 16) : (a >> 16));
+                  red_add_shared(Hs + lo_off + (w4[e] & 0xffffu), h ? -(a & 0xffff) : (a & 0xffff));
+                }
+                if (row + s1 < p.rows) {
+                  red_add_shared(Hs + (w4[e] >> 16), h ? -(c >> 16) : (c >> 16));
+                  red_add_shared(Hs + lo_off + (w4[e] >> 16), h ? -(c & 0xffff) : (c & 0xffff));
+                }
+              } else {
+                if (row + s0 < p.rows) red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
+                if (row + s1 < p.rows) red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
+              }
             }
           }
         }
@@ -351,16 +401,20 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     if (lb < 0) lb = 0;
     const int fbase = (fw * 32 + lane) << lb;
     const bool active = fbase < nbk;
-    int32_t prev[MAXNH];
+    int32_t prev[LIMBS][MAXNH];
 #pragma unroll
-    for (int i = 0; i < MAXNH; ++i) prev[i] = 0;
-    for (int f = 0; f < nunits; ++f) {
-      const int fb = f % NH;
-      const int32_t* H = hist + fb * nbk;
-      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 3);
-      mbar_wait(&hfull[fb], (uint32_t)((f / NH) & 1));
-      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 4);
-      // my bins: 2^lb <= 128 logical bins, same swizzle constant per 32-bin group
+    for (int l = 0; l < LIMBS; ++l)
+#pragma unroll
+      for (int i = 0; i < MAXNH; ++i) prev[l][i] = 0;
+    int fx_e = 0;
+    if constexpr (FX) fx_e = fx_exponent(fxmax, nwarps);
+    // slot of lane i: 0-7 local bits (< lb), 8-12 lane bits, 13-14 fold-warp bits
+    int sh = -1;
+    if (lane < 8) sh = lane < lb ? lane : -1;
+    else if (lane < 13) sh = lb + (lane - 8);
+    else if (lane < 15) sh = lb + 5 + (lane - 13);
+    // per-lane partials of my bins of one limb histogram, then REDUX over the warp: lane i -> slot i
+    auto fold_limb = [&](const int32_t* H) -> int32_t {
       int32_t a[8];  // local-bit partials, lb <= 7
 #pragma unroll
       for (int i = 0; i < 8; ++i) a[i] = 0;
@@ -418,10 +472,6 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
             }
         }
       }
-      __syncwarp();
-      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 5);
-      if (lane == 0) mbar_arrive(&hfree[fb]);  // release: my reads of the buffer are complete
-      // slot i: 0-7 local bits (< lb), 8-12 lane bits, 13-14 fold-warp bits; lane i keeps slot i
       int32_t r = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -437,17 +487,43 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       const int32_t W = __reduce_add_sync(0xffffffffu, X);
       if (lane == 13) r = (fw & 1) ? W : 0;
       if (lane == 14) r = (fw & 2) ? W : 0;
-      int32_t pv = 0;
+      return r;
+    };
+    for (int f = 0; f < nunits; ++f) {
+      const int fb = f % NH;
+      const int32_t* H = hist + fb * LIMBS * nbk;
+      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 3);
+      mbar_wait(&hfull[fb], (uint32_t)((f / NH) & 1));
+      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 4);
+      int32_t d[LIMBS];  // this block's slot value per limb: fold(H now) - fold(H after block f - NH)
 #pragma unroll
-      for (int i = 0; i < MAXNH; ++i)
-        if (i == fb) { pv = prev[i]; prev[i] = r; }
-      int sh = -1;
-      if (lane < 8) sh = lane < lb ? lane : -1;
-      else if (lane < 13) sh = lb + (lane - 8);
-      else if (lane < 15) sh = lb + 5 + (lane - 13);
+      for (int l = 0; l < LIMBS; ++l) {
+        const int32_t r = fold_limb(H + l * nbk);
+        int32_t pv = 0;
+#pragma unroll
+        for (int i = 0; i < MAXNH; ++i)
+          if (i == fb) { pv = prev[l][i]; prev[l][i] = r; }
+        d[l] = r - pv;
+      }
+      __syncwarp();
+      if (fw == 0 && f < 40) TRACE(8 + f * 8 + 5);
+      if (lane == 0) mbar_arrive(&hfree[fb]);  // release: my reads of the buffer are complete
       const int b = p.b_begin + col_cta + f * ncol;
       const int w = block_width(p.cols, p.k, b);
-      if (sh >= 0 && sh < w && r != pv) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)(r - pv));
+      if constexpr (FX) {
+        // exact fixed-point slot values from the 4 fold warps, summed in a fixed order
+        long long* fp = fxpart + (f & 1) * kFoldWarps * 16;
+        if (lane < 16) fp[fw * 16 + lane] = ((long long)d[0] << 16) + (long long)d[LIMBS - 1];
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kFoldWarps) : "memory");
+        if (fw == 0 && sh >= 0 && sh < w) {
+          long long tot = 0;
+#pragma unroll
+          for (int i = 0; i < kFoldWarps; ++i) tot += fp[i * 16 + lane];
+          out[(int64_t)b * p.k + (w - 1 - sh)] = (OutT)ldexp((double)tot, -fx_e);
+        }
+      } else {
+        if (sh >= 0 && sh < w && d[0] != 0) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)d[0]);
+      }
       if (fw == 0 && f < 40) TRACE(400 + f);
     }
   }
@@ -491,8 +567,10 @@ __device__ __forceinline__ T vload(const T* vs, const T* vg, uint32_t row, bool 
 // pattern (one (bucket, total) record per window, expanded in parallel at the range end).
 // Everything is linear, so the warps' partial column sums are combined in a fixed order:
 // deterministic, no float atomics.
-template <typename T, bool FOLDPP>
+template <typename T, bool FOLDPP, bool PERM16>
 __global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherParams p) {
+  constexpr int AHEAD = PERM16 ? 12 : 6;  // perm windows in flight per warp (16-byte loads)
+  constexpr int PW = PERM16 ? 1 : 2;      // uint4 per lane per window
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int seg_words = p.seg_in_smem ? (int)((p.seg_stride + 3) & ~3) : 0;
@@ -551,42 +629,43 @@ __global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherP
       T carry = T(0);
       const uint16_t* perm16 = reinterpret_cast<const uint16_t*>(perm_g) + (int64_t)b * p.row_stride;
       const uint32_t* perm32 = reinterpret_cast<const uint32_t*>(perm_g) + (int64_t)b * p.row_stride;
-      auto load_perm = [&](int w0, uint4 (&q)[2]) {
+      auto load_perm = [&](int w0, uint4 (&q)[PW]) {
         const int pos0 = w0 + 8 * lane;
-        q[0] = q[1] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int i = 0; i < PW; ++i) q[i] = make_uint4(0, 0, 0, 0);
         if (pos0 < P1) {
-          if (p.perm_bytes == 2) {
+          if (PERM16) {
             q[0] = ld_nc_v4(perm16 + pos0);
           } else {
             q[0] = ld_nc_v4(perm32 + pos0);
-            q[1] = ld_nc_v4(perm32 + pos0 + 4);
+            q[PW - 1] = ld_nc_v4(perm32 + pos0 + 4);
           }
         }
       };
-      uint4 ring[kPermAhead][2];
+      uint4 ring[AHEAD][PW];
 #pragma unroll
-      for (int i = 0; i < kPermAhead; ++i) load_perm(P0 + 256 * i, ring[i]);
-      for (int wb = P0; wb < P1; wb += 256 * kPermAhead) {
+      for (int i = 0; i < AHEAD; ++i) load_perm(P0 + 256 * i, ring[i]);
+      for (int wb = P0; wb < P1; wb += 256 * AHEAD) {
 #pragma unroll
-        for (int ri = 0; ri < kPermAhead; ++ri) {  // static ring slots: no register shuffling
+        for (int ri = 0; ri < AHEAD; ++ri) {  // static ring slots: no register shuffling
           const int w0 = wb + 256 * ri;
           if (w0 < P1) {
             const int E = min(256, P1 - w0);
             const int pos0 = w0 + 8 * lane;
             uint32_t rowsel[8];
-            if (p.perm_bytes == 2) {
+            if (PERM16) {
               const uint4 q0 = ring[ri][0];
               rowsel[0] = q0.x & 0xffffu; rowsel[1] = q0.x >> 16; rowsel[2] = q0.y & 0xffffu; rowsel[3] = q0.y >> 16;
               rowsel[4] = q0.z & 0xffffu; rowsel[5] = q0.z >> 16; rowsel[6] = q0.w & 0xffffu; rowsel[7] = q0.w >> 16;
             } else {
-              const uint4 q0 = ring[ri][0], q1 = ring[ri][1];
+              const uint4 q0 = ring[ri][0], q1 = ring[ri][PW - 1];
               rowsel[0] = q0.x; rowsel[1] = q0.y; rowsel[2] = q0.z; rowsel[3] = q0.w;
               rowsel[4] = q1.x; rowsel[5] = q1.y; rowsel[6] = q1.z; rowsel[7] = q1.w;
             }
             T x[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) x[e] = (pos0 + e < P1) ? vload(vs, vg, rowsel[e], vsm) : T(0);
-            load_perm(w0 + 256 * kPermAhead, ring[ri]);  // refill this slot
+            load_perm(w0 + 256 * AHEAD, ring[ri]);  // refill this slot
 #pragma unroll
             for (int e = 1; e < 8; ++e) x[e] += x[e - 1];
             const T incl = warp_inclusive_scan(x[7], lane);
@@ -762,9 +841,9 @@ static bool pdl_enabled() {
   return on == 1;
 }
 
-template <bool PP, typename OutT>
+template <bool PP, typename OutT, bool FX>
 rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
-  auto kern = p.halves == 2 ? scatter_kernel<kScatterR, PP, true, OutT> : scatter_kernel<kScatterR, PP, false, OutT>;
+  auto kern = p.halves == 2 ? scatter_kernel<kScatterR, PP, true, OutT, FX> : scatter_kernel<kScatterR, PP, false, OutT, FX>;
   rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "scatter smem attribute");
   if (st != RSR_OK) return st;
@@ -781,12 +860,12 @@ rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int t
   return cuda_check(cudaLaunchKernelEx(&cfg, kern, p), "scatter_kernel launch");
 }
 
-rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out, rsr_dtype out_dtype, bool pp,
+rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, void* out, rsr_dtype out_dtype, bool pp,
                             int b0, int b1, cudaStream_t s) {
   if (d.k > 14) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply supports k <= 14");
   ScatterParams p{};
   for (int h = 0; h < d.halves; ++h) p.key[h] = d.half[h].bucket;
-  p.v = v;
+  p.v = reinterpret_cast<const int32_t*>(v);
   p.v_aligned = ((uintptr_t)v & 15) == 0;
   p.out = out;
   p.rows = d.rows;
@@ -808,9 +887,11 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
   p.atomic_out = p.n_splits > 1;
   const size_t slot_bytes = (size_t)d.halves * p.rows_per_cta * 2;
   const size_t max_smem = device_max_smem_optin();
-  auto need = [&](int st, int nh) {
-    return ((sizeof(int32_t) * ((((size_t)1 << d.k) * nh + 15) & ~(size_t)15) + 127) & ~(size_t)127) +
-           st * slot_bytes + 8 * ((threads / 32) * st + 2 * nh) + 64;  // + fold warps: no smem
+  const size_t limbs = fx ? 2 : 1;
+  auto need = [&](int st, int nh) {  // layout of scatter_kernel's dynamic smem
+    return ((sizeof(int32_t) * ((((size_t)1 << d.k) * nh * limbs + 15) & ~(size_t)15) + 127) & ~(size_t)127) +
+           st * slot_bytes + 8 * ((threads / 32) * st + 2 * nh) + 64 /* fxmax */ +
+           (fx ? sizeof(long long) * 2 * kFoldWarps * 16 : 0) /* fxpart */;
   };
   // prefer >= 3 ring stages, then a third histogram buffer, then a 4th stage
   int stages = 0, nhist = 0;
@@ -837,11 +918,14 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const int32_t* v, void* out
     rsr_status st = cuda_check(cudaMemsetAsync((char*)out + c0 * esz, 0, (c1 - c0) * esz, s), "memset out");
     if (st != RSR_OK) return st;
   }
+  if (fx)
+    return pp ? launch_scatter_t<true, float, true>(p, grid, smem, threads, s)
+              : launch_scatter_t<false, float, true>(p, grid, smem, threads, s);
   if (out_dtype == RSR_F64)
-    return pp ? launch_scatter_t<true, double>(p, grid, smem, threads, s)
-              : launch_scatter_t<false, double>(p, grid, smem, threads, s);
-  return pp ? launch_scatter_t<true, int32_t>(p, grid, smem, threads, s)
-            : launch_scatter_t<false, int32_t>(p, grid, smem, threads, s);
+    return pp ? launch_scatter_t<true, double, false>(p, grid, smem, threads, s)
+              : launch_scatter_t<false, double, false>(p, grid, smem, threads, s);
+  return pp ? launch_scatter_t<true, int32_t, false>(p, grid, smem, threads, s)
+            : launch_scatter_t<false, int32_t, false>(p, grid, smem, threads, s);
 }
 
 template <typename T>
@@ -877,7 +961,8 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
   const int per_sm = std::max<int>(1, (int)std::min<size_t>(4, (228u << 10) / (smem + 1024)));
   const int nblk = b1 - b0;
   const int grid = std::max(1, std::min(nblk, device_sm_count() * per_sm));
-  auto kern = pp ? gather_kernel<T, true> : gather_kernel<T, false>;
+  auto kern = d.perm_bytes == 2 ? (pp ? gather_kernel<T, true, true> : gather_kernel<T, false, true>)
+                                : (pp ? gather_kernel<T, true, false> : gather_kernel<T, false, false>);
   rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "gather smem attribute");
   if (st != RSR_OK) return st;
@@ -891,11 +976,18 @@ rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* 
                     rsr_form form, int b0, int b1, cudaStream_t s) {
   const bool pp = var == RSR_VARIANT_RSRPP;
   if (b0 >= b1) return RSR_OK;
-  if (form == RSR_FORM_AUTO) form = (vt == RSR_I32 && d.k <= 14) ? RSR_FORM_SCATTER : RSR_FORM_GATHER;
+  // fp32 on the scatter kernel needs one quantization scale per output column: one row split
+  const bool fx_ok = vt == RSR_F32 && ot == RSR_F32 && d.rows <= (int64_t)kScatterThreads * kScatterR && d.k <= 14;
+  if (form == RSR_FORM_AUTO)
+    form = ((vt == RSR_I32 && d.k <= 14) || fx_ok) ? RSR_FORM_SCATTER : RSR_FORM_GATHER;
   if (form == RSR_FORM_SCATTER) {
-    if (vt != RSR_I32) return fail(RSR_ERR_INVALID, "scatter form needs int32 activations");
+    if (vt == RSR_F32) {
+      if (!fx_ok) return fail(RSR_ERR_INVALID, "fp32 scatter form needs rows <= 16384, k <= 14, fp32 output");
+      return multiply_scatter(d, v, true, out, ot, pp, b0, b1, s);
+    }
+    if (vt != RSR_I32) return fail(RSR_ERR_INVALID, "scatter form needs int32 or fp32 activations");
     if (ot != RSR_I32 && ot != RSR_F64) return fail(RSR_ERR_INVALID, "int32 activations produce int32 or float64");
-    return multiply_scatter(d, (const int32_t*)v, out, ot, pp, b0, b1, s);
+    return multiply_scatter(d, v, false, out, ot, pp, b0, b1, s);
   }
   if (vt != ot) return fail(RSR_ERR_INVALID, "gather form writes the activation dtype");
   switch (vt) {

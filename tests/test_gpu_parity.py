@@ -256,3 +256,25 @@ def test_block_products_bitwise(rsr, cuda, folds):
             u = rsr.SegmentedSums(w, folds[f"w{w}{tag}_u"])
             assert rsr.block_product_rsrpp(u).tobytes() == folds[f"w{w}{tag}_rsrpp"].tobytes()
             assert rsr.block_product_rsr(u).tobytes() == folds[f"w{w}{tag}_rsr"].tobytes()
+
+
+def test_fp32_fixed_point_scatter_deterministic(rsr, cuda):
+    """fp32 activations on the scatter kernel (exact two-limb fixed-point accumulation):
+    within the north-star tolerance of the fp64 oracle and bitwise reproducible."""
+    import torch
+    from paper_2411_06360_b200 import kernels as K, _native
+    for rows, cols, k in ((300, 77, 6), (4096, 1000, 9), (16384, 400, 11), (5000, 64, 12)):
+        rng = np.random.default_rng([rows, cols, 32])
+        A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        vf = (rng.standard_normal(rows) * 3).astype(np.float32)
+        tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+        ref = vf.astype(np.float64) @ A.astype(np.float64)
+        dv = torch.from_numpy(vf).cuda()
+        a = K._multiply_device(dv, tidx, True, form=_native.FORM_SCATTER).cpu().numpy()
+        b = K._multiply_device(dv, tidx, True, form=_native.FORM_SCATTER).cpu().numpy()
+        assert a.tobytes() == b.tobytes()
+        assert _fp32_ok(a, ref), float(np.abs(a - ref).max())
+        g = K._multiply_device(dv, tidx, False, form=_native.FORM_GATHER).cpu().numpy()
+        assert _fp32_ok(g, ref)
+        auto = rsr.multiply_ternary(dv, tidx).cpu().numpy()
+        assert _fp32_ok(auto, ref)
