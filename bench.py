@@ -169,6 +169,28 @@ def time_cpu_reference(A: np.ndarray, v: np.ndarray, k: int, domain: str, min_se
     return float(np.mean(samples)), len(samples), workers, out
 
 
+def time_cpu_extras(A: np.ndarray, v: np.ndarray, k: int, domain: str, budget_s: float = 6.0):
+    """the same C port on ONE thread, and the reference's standard dense
+    multiply (core.py:135-169, C port `naive_ternary`), each a bounded sample."""
+    from oracle import c_oracle
+    n, m = A.shape
+    kp = c_oracle.keys_ternary(A, k, 1)
+    kn = c_oracle.keys_ternary(A, k, -1) if domain == "ternary" else None
+    v64 = v.astype(np.float64)
+    res = {}
+    for name, run in (("rsrpp_1thread", lambda: c_oracle.multiply_parallel(v64, kp, kn, m, k, True, 1)),
+                      ("standard_1thread", lambda: c_oracle.naive_ternary(v64, A))):
+        run()
+        samples = []
+        t_end = time.perf_counter() + budget_s / 2
+        while time.perf_counter() < t_end or not samples:
+            t0 = time.perf_counter()
+            run()
+            samples.append(time.perf_counter() - t0)
+        res[name] = {"value": 1.0 / float(np.mean(samples)), "unit": "vectors/s", "cores": 1, "reps": len(samples)}
+    return res
+
+
 def run_reference(args, cfg):
     """--impl reference: rank 0 only, the C port of the reference CPU path."""
     rank = int(os.environ.get("RANK", "0"))
@@ -354,7 +376,9 @@ def run_ours(args, cfg):
 
     peak, peak_kind = _peaks()
     avg_kernel_s = statistics.mean(kernel_ms) / 1e3
-    achieved = read_bytes / avg_kernel_s / 1e9
+    # roofline.achieved counts the CANONICAL algorithmic bytes (u16 perm +
+    # u32 seg per block and half, + v + out); our index encoding reads fewer (index_bytes)
+    achieved = canonical / avg_kernel_s / 1e9
     line = {
         "metric": "ternary RSR++ matvec vectors/sec" if domain == "ternary" else "binary RSR++ matvec vectors/sec",
         "value": value, "unit": "vectors/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
@@ -368,9 +392,9 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": 8 * m, "path": "rsr.multiply_ternary(numpy int32 v, idx)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _profile_traffic(args.config),
-                     "peak_kind": peak_kind, "algorithmic_bytes": read_bytes,
-                     "canonical_gather_bytes": canonical,
-                     "canonical_gbs": canonical / avg_kernel_s / 1e9,
+                     "peak_kind": peak_kind, "algorithmic_bytes": canonical,
+                     "bytes_definition": "SURVEY.md 8(d) canonical: sum over halves, blocks of 2n + 4*2^w, + 4n + 4m",
+                     "index_bytes": read_bytes, "index_gbs": read_bytes / avg_kernel_s / 1e9,
                      "kernel_us": avg_kernel_s * 1e6},
         "clocks": clocks.summary(),
     }
@@ -380,6 +404,7 @@ def run_ours(args, cfg):
         line["cpu_baseline"] = {"value": 1.0 / cpu_s, "unit": "vectors/s", "cores": workers, "kind": "port",
                                 "sample": f"{reps} full {n}x{m} RSR++ matvecs, fp64, C port of "
                                           "kernels.py:127-239 on {workers} threads".replace("{workers}", str(workers))}
+        line["cpu_baseline"].update(time_cpu_extras(make_matrix(domain, n, m), v, k, domain))
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

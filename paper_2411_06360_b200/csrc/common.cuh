@@ -73,6 +73,40 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+// Key-order schedule of the scatter kernel (k <= 11, csrc/preprocess.cu schedule_keys_kernel).
+// Inside an aligned 8-row group the codes are stored in slot order; slot s holds row p[s]
+// where p = butterfly8(identity, ctrl).  The 12 control bits live in bits 13-15 of the
+// group's codes 0..3 (codes are <= 8188 for k <= 11): bits 3c..3c+2 in code c.
+constexpr uint32_t kSchedCodeMask = 0x1fff1fffu;  // clears the control bits of two codes
+
+__device__ __forceinline__ uint32_t sched_ctrl(uint32_t w0, uint32_t w1) {
+  return ((w0 >> 13) & 7u) | ((w0 >> 26) & 0x38u) | (((w1 >> 13) & 7u) << 6) | ((w1 >> 20) & 0xe00u);
+}
+
+// Butterfly network on 8 values: stage st (0..2) swaps a[e] and a[e | 1 << st] for the four
+// e with bit st clear (switch i = their rank) when control bit 4*st + i is set.
+template <typename T>
+__device__ __forceinline__ void butterfly8(T (&a)[8], uint32_t ctrl) {
+#pragma unroll
+  for (int st = 0; st < 3; ++st) {
+    int i = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (!(e & (1 << st))) {
+        const bool sw = (ctrl >> (4 * st + i)) & 1u;
+        const T x = a[e], y = a[e | (1 << st)];
+        a[e] = sw ? y : x;
+        a[e | (1 << st)] = sw ? x : y;
+        ++i;
+      }
+  }
+}
+
+// Bulk prefetch of [src, src + bytes) into L2 (bytes % 16 == 0, src 16-byte aligned).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

@@ -30,6 +30,7 @@
 //    floating-point atomics: results are deterministic run to run.
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -103,8 +104,8 @@ struct ScatterParams {
   int rows_per_cta, n_splits, stages, atomic_out, nhist;
   int v_aligned;
   int scatter_warps;
-  int sched;          // keys stored in scheduled order (k <= 11): x in bits 13-15 of each group's first code
-  uint32_t lo_mask;   // mask of the first code word's low half (clears the x bits)
+  int sched;          // keys stored in scheduled order (k <= 11): butterfly control bits in the codes
+  uint32_t code_mask; // mask of the group's first two code words (clears the control bits)
 };
 
 template <typename OutT>
@@ -134,10 +135,12 @@ __device__ __forceinline__ int4 unswizzle4(int4 q, uint32_t c) {
 // Persistent CTA (one per SM at n >= 8192): up to 16 SCATTER warps + kFoldWarps FOLD warps.
 //  * Scatter warp w, lane l owns rows w*32R + 256g + 8l + e (g < R/8, e < 8) of the CTA's row
 //    slice: their v values live in registers for the whole launch.  Each scatter warp streams
-//    its rows' key codes of every column block through a private S-slot shared-memory ring
-//    with 1-D TMA bulk copies (lane 0 issues, per-warp mbarriers) and refills a slot as soon
-//    as it has read it.  Key reads are conflict-free 16-byte loads, software-pipelined one
-//    half-block ahead, so the reductions of one half hide the load latency of the next.
+//    its rows' key codes of every column block straight into registers (16-byte
+//    ld.global.nc.L1::no_allocate per 8 rows, software-pipelined one half-block ahead) while
+//    lane 0 keeps S blocks ahead with cp.async.bulk.prefetch.L2, so the register loads hit L2.
+//    Keys never touch shared memory: the smem data path (128 B/clk) is the kernel's bound and
+//    belongs to the reductions (tools/microbench/red_stream.cu: TMA->smem->LDS streaming
+//    costs 1.5x the LDG path against concurrent REDs).
 //  * Both halves of a ternary index scatter into ONE 2^k-bin histogram (+v for the positive
 //    key, -v for the negative key): the fold is linear, so fold(u+ - u-) is exactly the
 //    reference's `pos - neg` (kernels.py:206) in integer arithmetic.
@@ -164,7 +167,7 @@ __device__ __forceinline__ int fx_exponent(const uint32_t* fxmax, int n) {
 // 16-bit limbs in two int32 histograms (integer atomics are native; fp32 shared atomics are a
 // CAS loop on sm_100).  Deterministic, and more accurate than fp32 summation.  Single row
 // split only (one scale per output column).
-template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX>
+template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, bool SCHED>
 __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
   static_assert(R % 8 == 0 && R * kScatterThreads <= 16384, "rows per CTA");
   constexpr int LIMBS = FX ? 2 : 1;
@@ -181,9 +184,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   const int NH = p.nhist;
   const int hist_words = (NH * LIMBS * nbk + 15) & ~15;
   int32_t* hist = reinterpret_cast<int32_t*>(smem);  // [NH][LIMBS][nbk]
-  uint16_t* ring_all = reinterpret_cast<uint16_t*>(smem + ((sizeof(int32_t) * hist_words + 127) & ~(size_t)127));
-  uint64_t* wfull_all = reinterpret_cast<uint64_t*>(ring_all + (size_t)nwarps * S * HALVES * WROWS);
-  uint64_t* hfull = wfull_all + nwarps * S;
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + ((sizeof(int32_t) * hist_words + 127) & ~(size_t)127));
   uint64_t* hfree = hfull + NH;
   uint32_t* fxmax = reinterpret_cast<uint32_t*>(hfree + NH);                   // [16] per-warp max |v| bits
   long long* fxpart = reinterpret_cast<long long*>(fxmax + 16);                // [2][kFoldWarps][16]
@@ -201,25 +202,15 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   if (warp == 0) TRACE(0);
 
   // ---- prologue (index only: may overlap the previous kernel under PDL) ----
-  uint16_t* ring = ring_all + (size_t)(is_fold ? 0 : warp) * S * HALVES * WROWS;  // my [S][HALVES][WROWS]
-  uint64_t* wfull = wfull_all + (is_fold ? 0 : warp) * S;
   const int64_t wr0 = r0 + (int64_t)warp * WROWS;  // first row of this (scatter) warp
   const int wcopy = is_fold ? 0 : (int)std::max<int64_t>(0, std::min<int64_t>(WROWS, p.row_stride - wr0));
-  const uint32_t wbytes = (uint32_t)wcopy * 2u;
-  uint64_t policy = 0;
-  if (lane == 0 && !is_fold) {
-    for (int s = 0; s < S; ++s) mbar_init(&wfull[s], 1);
-    fence_mbar_init();
-    policy = l2_evict_first_policy();
-    for (int u = 0; u < S && u < nunits; ++u) {
-      const int b = p.b_begin + col_cta + u * ncol;
-      mbar_arrive_expect_tx(&wfull[u], wbytes * HALVES);
-      if (wbytes)
-        for (int h = 0; h < HALVES; ++h)
-          tma_load_1d(ring + ((size_t)u * HALVES + h) * WROWS, (h ? key1 : key0) + (int64_t)b * p.row_stride + wr0,
-                      wbytes, &wfull[u], policy);
-    }
-  }
+  const uint32_t wbytes = (uint32_t)wcopy * 2u;  // multiple of 16 (row_stride % 8 == 0)
+  auto prefetch_unit = [&](int u) {              // lane 0: both halves of unit u into L2
+    const int b = p.b_begin + col_cta + u * ncol;
+    for (int h = 0; h < HALVES; ++h) prefetch_l2_bulk((h ? key1 : key0) + (int64_t)b * p.row_stride + wr0, wbytes);
+  };
+  if (lane == 0 && !is_fold && wbytes)
+    for (int u = 0; u <= S && u < nunits; ++u) prefetch_unit(u);  // before the PDL wait
   if (t == 0) {
     for (int h = 0; h < NH; ++h) {
       mbar_init(&hfull[h], nwarps);
@@ -239,11 +230,23 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 
   if (!is_fold) {
     // =========================== scatter warps ===========================
-    const bool all_valid = wr0 + 256 * (NG - 1) + 8 * lane + 8 <= p.rows;
-    const bool warp_all_valid = wr0 + 256 * (NG - 1) + 256 <= p.rows;  // every lane of the warp
-    const bool warp_none = wr0 >= p.rows;                                // a padding warp
+    const bool warp_all_valid = wr0 + WROWS <= p.rows;  // every row of this warp is a matrix row
     const uint32_t hist_s = smem_u32(hist);
-    const uint32_t ring_s = smem_u32(ring);
+    // this lane's keys of 8-row group g of unit u, half h: kb[h] + u * ustride + 256 g
+    const int64_t ustride = (int64_t)ncol * p.row_stride;
+    const int64_t koff = (int64_t)(p.b_begin + col_cta) * p.row_stride + wr0 + 8 * lane;
+    const uint16_t* kb0 = key0 + koff;
+    const uint16_t* kb1 = TERNARY ? key1 + koff : nullptr;
+    uint32_t gmask = 0;  // groups present in the key arrays (all but in the last warp)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) gmask |= (wr0 + 256 * g + 8 * lane < p.row_stride) ? (1u << g) : 0u;
+    uint4 q0[NG], q1[NG];  // the current unit's keys; refilled group by group with the next unit's
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const bool ld = nunits > 0 && ((gmask >> g) & 1u);
+      q0[g] = ld ? ld_nc_v4(kb0 + 256 * g) : make_uint4(0, 0, 0, 0);
+      q1[g] = (TERNARY && ld) ? ld_nc_v4(kb1 + 256 * g) : make_uint4(0, 0, 0, 0);
+    }
     int32_t vr[R];
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         vr[8 * g + 4] = c.x; vr[8 * g + 5] = c.y; vr[8 * g + 6] = c.z; vr[8 * g + 7] = c.w;
       } else {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;
+        for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;  // rows past the end: 0
       }
     }
     if constexpr (FX) {  // CTA max |v| -> quantization scale
@@ -273,123 +276,71 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       for (int i = 0; i < R; ++i) vr[i] = __float2int_rn(ldexpf(__int_as_float(vr[i]), e));
     }
     if (warp == 0) TRACE(1);
-    auto load_keys = [&](int slot, int h, uint4 (&q)[NG]) {
-      const uint32_t base = ring_s + (uint32_t)(((slot * HALVES + h) * WROWS + 8 * lane) * 2);
+    constexpr uint32_t kMask = SCHED ? kSchedCodeMask : 0xffffffffu;
+    // the reductions of one half of one group: slot s adds +-vp[s] into the bin of code s.
+    // SKIP0 (the warp holding the end of the rows): rows past the end carry v = 0 and their
+    // (padding or absent) codes are skipped; a zero contribution is a no-op for any row.
+    auto reduce_group = [&](uint32_t Hs, const uint4& a, const int32_t (&vp)[8], bool neg, auto skip0) {
+      constexpr bool SKIP0 = decltype(skip0)::value;
+      const uint32_t w4[4] = {a.x & kMask, a.y & kMask, a.z, a.w};
 #pragma unroll
-      for (int g = 0; g < NG; ++g) q[g] = ld_shared_v4(base + (uint32_t)(g * 512));
+      for (int e = 0; e < 4; ++e) {
+        const int32_t x0 = vp[2 * e], x1 = vp[2 * e + 1];
+        const uint32_t c0 = w4[e] & 0xffffu, c1 = w4[e] >> 16;
+        if constexpr (FX) {
+          const uint32_t lo_off = (uint32_t)nbk * 4u;
+          if (!SKIP0 || x0 != 0) {
+            red_add_shared(Hs + c0, neg ? -(x0 >> 16) : (x0 >> 16));
+            red_add_shared(Hs + lo_off + c0, neg ? -(x0 & 0xffff) : (x0 & 0xffff));
+          }
+          if (!SKIP0 || x1 != 0) {
+            red_add_shared(Hs + c1, neg ? -(x1 >> 16) : (x1 >> 16));
+            red_add_shared(Hs + lo_off + c1, neg ? -(x1 & 0xffff) : (x1 & 0xffff));
+          }
+        } else {
+          if (!SKIP0 || x0 != 0) red_add_shared(Hs + c0, neg ? -x0 : x0);
+          if (!SKIP0 || x1 != 0) red_add_shared(Hs + c1, neg ? -x1 : x1);
+        }
+      }
     };
-    uint4 q[NG];
-    if (nunits > 0) {
-      mbar_wait(&wfull[0], 0);
-      load_keys(0, 0, q);
-    }
     for (int u = 0; u < nunits; ++u) {
       if (u + 1 == nunits) grid_launch_dependents();  // the next grid may start its prologue on freed SMs
-      const int slot = u % S;
       const int hb = u % NH;
+      if (lane == 0 && wbytes && u + 1 + S < nunits) prefetch_unit(u + 1 + S);
       const uint32_t Hs = hist_s + (uint32_t)(hb * LIMBS * nbk) * 4u;
       if (warp == 0 && u < 40) TRACE(8 + u * 8 + 0);
       if (u >= NH) mbar_wait(&hfree[hb], (uint32_t)(((u / NH) - 1) & 1));
       if (warp == 0 && u < 40) TRACE(8 + u * 8 + 1);
+      const bool more = u + 1 < nunits;
+      kb0 += ustride;
+      if constexpr (TERNARY) kb1 += ustride;
 #pragma unroll
-      for (int h = 0; h < HALVES; ++h) {
-        uint4 qn[NG];  // next half-block's keys, loaded before this half's reductions
-        if (h + 1 < HALVES) {
-          load_keys(slot, h + 1, qn);
-        } else if (u + 1 < nunits) {
-          const int ns = (u + 1) % S;
-          mbar_wait(&wfull[ns], (uint32_t)(((u + 1) / S) & 1));
-          load_keys(ns, 0, qn);
+      for (int g = 0; g < NG; ++g) {
+        const uint4 a0 = q0[g];
+        const uint4 a1 = q1[g];
+        if (more && ((gmask >> g) & 1u)) {  // the next unit's keys of this group: a whole unit ahead
+          q0[g] = ld_nc_v4(kb0 + 256 * g);
+          if constexpr (TERNARY) q1[g] = ld_nc_v4(kb1 + 256 * g);
+        }
+        // slot s of the group holds row p[s], p = butterfly of the control bits (k <= 11):
+        // route the v registers the same way, once for both halves
+        int32_t vp[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) vp[e] = vr[g * 8 + e];
+        if constexpr (SCHED) butterfly8(vp, sched_ctrl(a0.x, a0.y));
+        if (warp_all_valid) {
+          reduce_group(Hs, a0, vp, false, std::false_type{});
+          if constexpr (TERNARY) reduce_group(Hs, a1, vp, true, std::false_type{});
         } else {
-#pragma unroll
-          for (int g = 0; g < NG; ++g) qn[g] = make_uint4(0, 0, 0, 0);
+          reduce_group(Hs, a0, vp, false, std::true_type{});
+          if constexpr (TERNARY) reduce_group(Hs, a1, vp, true, std::true_type{});
         }
-        if (warp_none) {
-        } else if (warp_all_valid) {
-#pragma unroll
-          for (int g = 0; g < NG; ++g) {
-            // scheduled key order (k <= 11): this lane processes its 8 rows in order e ^ x,
-            // x in bits 13-15 of the first code; permute the v registers to match (3 SEL stages)
-            const uint32_t x = p.sched ? (q[g].x >> 13) & 7u : 0u;
-            int32_t vp[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) vp[e] = vr[g * 8 + e];
-#pragma unroll
-            for (int st = 0; st < 3; ++st) {
-              const bool sw = (x >> st) & 1u;
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                if (!(e & (1 << st))) {
-                  const int32_t a = vp[e], c = vp[e | (1 << st)];
-                  vp[e] = sw ? c : a;
-                  vp[e | (1 << st)] = sw ? a : c;
-                }
-            }
-            const uint32_t w4[4] = {q[g].x & p.lo_mask, q[g].y, q[g].z, q[g].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int32_t a = vp[2 * e], c = vp[2 * e + 1];
-              if constexpr (FX) {
-                const uint32_t lo_off = (uint32_t)nbk * 4u;
-                red_add_shared(Hs + (w4[e] & 0xffffu), h ? -(a >> 16) : (a >> 16));
-                red_add_shared(Hs + lo_off + (w4[e] & 0xffffu), h ? -(a & 0xffff) : (a & 0xffff));
-                red_add_shared(Hs + (w4[e] >> 16), h ? -(c >> 16) : (c >> 16));
-                red_add_shared(Hs + lo_off + (w4[e] >> 16), h ? -(c & 0xffff) : (c & 0xffff));
-              } else {
-                red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
-                red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
-              }
-            }
-          }
-        } else {  // the warp holding the end of the rows: rows past it were never copied
-#pragma unroll
-          for (int g = 0; g < NG; ++g) {
-            const int64_t row = wr0 + 256 * g + 8 * lane;
-            const uint32_t x = p.sched ? (q[g].x >> 13) & 7u : 0u;
-            const uint32_t w4[4] = {q[g].x & p.lo_mask, q[g].y, q[g].z, q[g].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int s0 = (2 * e) ^ (int)x, s1 = (2 * e + 1) ^ (int)x;  // source rows in the group
-              int32_t a = 0, c = 0;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (i == s0) a = vr[g * 8 + i];
-                if (i == s1) c = vr[g * 8 + i];
-              }
-              if constexpr (FX) {
-                const uint32_t lo_off = (uint32_t)nbk * 4u;
-                if (row + s0 < p.rows) {
-                  red_add_shared(Hs + (w4[e] & 0xffffu), h ? -(a >> 16) : (a >> 16));
-                  red_add_shared(Hs + lo_off + (w4[e] & 0xffffu), h ? -(a & 0xffff) : (a & 0xffff));
-                }
-                if (row + s1 < p.rows) {
-                  red_add_shared(Hs + (w4[e] >> 16), h ? -(c >> 16) : (c >> 16));
-                  red_add_shared(Hs + lo_off + (w4[e] >> 16), h ? -(c & 0xffff) : (c & 0xffff));
-                }
-              } else {
-                if (row + s0 < p.rows) red_add_shared(Hs + (w4[e] & 0xffffu), h ? -a : a);
-                if (row + s1 < p.rows) red_add_shared(Hs + (w4[e] >> 16), h ? -c : c);
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int g = 0; g < NG; ++g) q[g] = qn[g];
       }
       __syncwarp();
       if (warp == 0 && u < 40) TRACE(8 + u * 8 + 2);
       if (lane == 0) {
         mbar_arrive(&hfull[hb]);  // release: this warp's reductions are visible to the fold warps
         if (warp == 0 && u < 40) TRACE(8 + u * 8 + 7);
-        if (u + S < nunits) {     // refill my slot (all its keys are in registers already)
-          const int bn = p.b_begin + col_cta + (u + S) * ncol;
-          mbar_arrive_expect_tx(&wfull[slot], wbytes * HALVES);
-          if (wbytes)
-            for (int h = 0; h < HALVES; ++h)
-              tma_load_1d(ring + ((size_t)slot * HALVES + h) * WROWS,
-                          (h ? key1 : key0) + (int64_t)bn * p.row_stride + wr0, wbytes, &wfull[slot], policy);
-        }
-        if (warp == 0 && u < 40) TRACE(300 + u);
       }
     }
   } else {
@@ -843,7 +794,10 @@ static bool pdl_enabled() {
 
 template <bool PP, typename OutT, bool FX>
 rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
-  auto kern = p.halves == 2 ? scatter_kernel<kScatterR, PP, true, OutT, FX> : scatter_kernel<kScatterR, PP, false, OutT, FX>;
+  auto kern = p.halves == 2 ? (p.sched ? scatter_kernel<kScatterR, PP, true, OutT, FX, true>
+                                       : scatter_kernel<kScatterR, PP, true, OutT, FX, false>)
+                            : (p.sched ? scatter_kernel<kScatterR, PP, false, OutT, FX, true>
+                                       : scatter_kernel<kScatterR, PP, false, OutT, FX, false>);
   rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "scatter smem attribute");
   if (st != RSR_OK) return st;
@@ -882,31 +836,29 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   p.rows_per_cta = threads * R;
   p.scatter_warps = threads / 32;
   p.sched = d.k <= 11;
-  p.lo_mask = p.sched ? 0xffff1fffu : 0xffffffffu;
+  p.code_mask = p.sched ? kSchedCodeMask : 0xffffffffu;
   p.n_splits = (int)((d.rows + p.rows_per_cta - 1) / p.rows_per_cta);
   p.atomic_out = p.n_splits > 1;
-  const size_t slot_bytes = (size_t)d.halves * p.rows_per_cta * 2;
   const size_t max_smem = device_max_smem_optin();
   const size_t limbs = fx ? 2 : 1;
-  auto need = [&](int st, int nh) {  // layout of scatter_kernel's dynamic smem
+  auto need = [&](int nh) {  // layout of scatter_kernel's dynamic smem
     return ((sizeof(int32_t) * ((((size_t)1 << d.k) * nh * limbs + 15) & ~(size_t)15) + 127) & ~(size_t)127) +
-           st * slot_bytes + 8 * ((threads / 32) * st + 2 * nh) + 64 /* fxmax */ +
-           (fx ? sizeof(long long) * 2 * kFoldWarps * 16 : 0) /* fxpart */;
+           8 * (2 * nh) + 64 /* fxmax */ + (fx ? sizeof(long long) * 2 * kFoldWarps * 16 : 0) /* fxpart */;
   };
-  // prefer >= 3 ring stages, then a third histogram buffer, then a 4th stage
-  int stages = 0, nhist = 0;
-  const int cand[][2] = {{3, 3}, {3, 2}, {4, 2}, {2, 2}, {2, 3}, {1, 2}};  // the deferred fold needs 2..3 buffers
-  for (auto& c : cand)
-    if (need(c[0], c[1]) <= max_smem) { stages = c[0]; nhist = c[1]; break; }
-  if (!stages) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: index slice does not fit in shared memory");
-  if (stages == 3 && nhist == 3 && need(4, 3) <= max_smem) stages = 4;
-  if (const char* e = getenv("RSR_B200_STAGES")) stages = atoi(e);  // diagnostics
+  // the deferred fold wants 3 histogram buffers (2 is the minimum)
+  int nhist = need(3) <= max_smem ? 3 : 2;
+  if (need(nhist) > max_smem) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: histograms do not fit in shared memory");
+  int stages = 3;  // L2 prefetch distance in blocks
+  if (const char* e = getenv("RSR_B200_STAGES")) stages = std::max(0, atoi(e));  // diagnostics
   if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::min(4, std::max(2, atoi(e)));
   p.stages = stages;
   p.nhist = nhist;
-  const size_t smem = need(stages, nhist);
-  // small CTAs (few rows) share an SM
-  const int per_sm = std::max<int>(1, (int)std::min<size_t>(2048 / (threads + 32 * kFoldWarps), (228u << 10) / (smem + 1024)));
+  const size_t smem = need(nhist);
+  // small CTAs (few rows) share an SM: limits from threads, smem and registers (<= 96 per
+  // thread under the launch bounds)
+  const int cta_threads = threads + 32 * kFoldWarps;
+  const int per_sm = std::max<int>(1, (int)std::min<size_t>(std::min(2048 / cta_threads, 65536 / (cta_threads * 96)),
+                                                            (228u << 10) / (smem + 1024)));
   const int nblk = b1 - b0;
   const int sms = device_sm_count();
   const int ncol = std::max(1, std::min(nblk, sms * per_sm / std::max(1, p.n_splits)));
