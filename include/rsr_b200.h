@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RSR_B200_ABI_VERSION 1
+#define RSR_B200_ABI_VERSION 2
 
 typedef enum rsr_status {
   RSR_OK = 0,
@@ -111,10 +111,18 @@ rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_d
                         rsr_dtype out_dtype, rsr_variant variant, rsr_form form,
                         int32_t block_begin, int32_t block_end, void* stream);
 
-/* Batched multiply: V [batch][rows] -> OUT [batch][cols] (same dtype rules). */
+/* Batched multiply: V [batch][rows] -> OUT [batch][cols] on the current stream, every index
+ * byte read once per slice of up to 128 vectors instead of once per vector (SURVEY.md §8(d)
+ * config 3; the reference has no batch API and runs `multiply_ternary`, kernels.py:196-206,
+ * once per vector).  int32 (exact) and fp32 activations run the batched gather kernel and
+ * need `workspace` of rsr_multiply_batched_workspace_bytes() bytes (device, 16-byte aligned;
+ * holds V transposed); out_dtype must equal v_dtype.  fp64 runs one multiply per vector
+ * (workspace unused). */
+size_t rsr_multiply_batched_workspace_bytes(const rsr_index_desc* desc, int64_t batch, rsr_dtype v_dtype);
 rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_dtype v_dtype,
                                 int64_t batch, void* OUT, rsr_dtype out_dtype,
-                                rsr_variant variant, void* stream);
+                                rsr_variant variant, void* workspace, size_t workspace_bytes,
+                                void* stream);
 
 /* End-to-end entry with HOST buffers (the call a reference-side binding makes):
  * copies v_host -> d_v, multiplies all blocks, copies d_out -> out_host and

@@ -18,13 +18,13 @@ I32, F32, F64 = 0, 1, 2
 VARIANT_RSR, VARIANT_RSRPP = 0, 1
 FORM_AUTO, FORM_SCATTER, FORM_GATHER = 0, 1, 2
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # Every symbol include/rsr_b200.h declares (tests check the .so exports them all).
 EXPORTS = (
     "rsr_b200_abi_version", "rsr_b200_last_error", "rsr_index_layout",
     "rsr_preprocess_workspace_bytes", "rsr_preprocess_ternary", "rsr_preprocess_binary",
-    "rsr_multiply", "rsr_multiply_batched", "rsr_multiply_host", "rsr_segmented_sum",
+    "rsr_multiply", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host", "rsr_segmented_sum",
     "rsr_block_product", "rsr_naive_multiply_ternary",
 )
 
@@ -75,8 +75,10 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, I32_, I32_, P]
     L.rsr_multiply.restype = st
+    L.rsr_multiply_batched_workspace_bytes.argtypes = [ctypes.POINTER(IndexDesc), I64, ctypes.c_int]
+    L.rsr_multiply_batched_workspace_bytes.restype = SZ
     L.rsr_multiply_batched.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, I64, P,
-                                       ctypes.c_int, ctypes.c_int, P]
+                                       ctypes.c_int, ctypes.c_int, P, SZ, P]
     L.rsr_multiply_batched.restype = st
     L.rsr_multiply_host.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                     ctypes.c_int, P, P, P]

@@ -1,5 +1,6 @@
 // extern "C" entry points of librsr_b200.so (declared in include/rsr_b200.h).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -19,6 +20,9 @@ rsr_status segmented_sum(const rsr_index_desc& d, int half, int block, const voi
 rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t lda, const void* v, rsr_dtype dt,
                          void* out, cudaStream_t s);
 rsr_status block_product(const double* u, int w, int use_fold, double* buf, double* out, cudaStream_t s);
+size_t batched_workspace_bytes(const rsr_index_desc& d, int64_t batch, rsr_dtype dt);
+rsr_status multiply_batched(const rsr_index_desc& d, const void* V, rsr_dtype vt, int64_t batch, void* out,
+                            rsr_dtype ot, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s);
 
 namespace {
 thread_local std::string g_last_error;
@@ -145,18 +149,39 @@ rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_d
   return multiply(*desc, v, v_dtype, out, out_dtype, variant, form, block_begin, block_end, (cudaStream_t)stream);
 }
 
+size_t rsr_multiply_batched_workspace_bytes(const rsr_index_desc* desc, int64_t batch, rsr_dtype v_dtype) {
+  return desc ? batched_workspace_bytes(*desc, batch, v_dtype) : 0;
+}
+
 rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_dtype v_dtype, int64_t batch, void* OUT,
-                                rsr_dtype out_dtype, rsr_variant variant, void* stream) {
+                                rsr_dtype out_dtype, rsr_variant variant, void* workspace, size_t workspace_bytes,
+                                void* stream) {
   rsr_status st = check_range(desc, 0, desc ? desc->nblocks : 0);
   if (st != RSR_OK) return st;
   if (batch < 0) return fail(RSR_ERR_INVALID, "batch must be non-negative");
-  const size_t vsz = v_dtype == RSR_F64 ? 8 : 4, osz = out_dtype == RSR_F64 ? 8 : 4;
-  for (int64_t i = 0; i < batch; ++i) {
-    st = multiply(*desc, (const char*)V + i * desc->rows * vsz, v_dtype, (char*)OUT + i * desc->cols * osz, out_dtype,
-                  variant, RSR_FORM_AUTO, 0, desc->nblocks, (cudaStream_t)stream);
-    if (st != RSR_OK) return st;
+  if (batch > 0 && (!V || !OUT)) return fail(RSR_ERR_INVALID, "null vector or output");
+  if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
+    return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
+  // int32 / fp32: the batched gather kernel reads the index once per slice of vectors; the
+  // per-vector scatter kernel re-reads it per vector but runs ~1.3x faster per vector while
+  // the index is L2-resident.  RSR_B200_BATCH_FORM=loop|gather overrides (diagnostics).
+  bool loop = v_dtype == RSR_F64;
+  if (!loop) {
+    const size_t index_bytes = (size_t)desc->halves * desc->nblocks * desc->row_stride * 2;
+    loop = index_bytes <= ((size_t)96 << 20) && desc->k <= 14 && out_dtype == v_dtype;
+    if (const char* e = getenv("RSR_B200_BATCH_FORM")) loop = e[0] == 'l';
   }
-  return RSR_OK;
+  if (loop) {  // one multiply per vector
+    const size_t vsz = v_dtype == RSR_F64 ? 8 : 4, osz = out_dtype == RSR_F64 ? 8 : 4;
+    for (int64_t i = 0; i < batch; ++i) {
+      st = multiply(*desc, (const char*)V + i * desc->rows * vsz, v_dtype, (char*)OUT + i * desc->cols * osz, out_dtype,
+                    variant, RSR_FORM_AUTO, 0, desc->nblocks, (cudaStream_t)stream);
+      if (st != RSR_OK) return st;
+    }
+    return RSR_OK;
+  }
+  return multiply_batched(*desc, V, v_dtype, batch, OUT, out_dtype, variant, workspace, workspace_bytes,
+                          (cudaStream_t)stream);
 }
 
 rsr_status rsr_multiply_host(const rsr_index_desc* desc, const void* v_host, rsr_dtype v_dtype, void* out_host,

@@ -16,6 +16,7 @@ of the sm_100a kernels in librsr_b200.so (see csrc/multiply.cu):
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -118,20 +119,24 @@ def _torch_dtype_code(t) -> int:
         raise ValueError("device vectors must be int32, float32 or float64") from None
 
 
-class _HostStaging:
-    """Pinned host buffers + device scratch reused by the host-buffer (e2e) path."""
+class _HostStaging(threading.local):
+    """Pinned host buffers + device scratch reused by the host-buffer (e2e) path.  Thread-local:
+    concurrent multiplies from several threads never share buffers."""
 
     def __init__(self):
         self.bufs = {}
 
     def get(self, key, shape, dtype, pinned):
+        """(tensor, numpy view or None, data pointer) of a cached buffer of `shape` elements."""
         import torch
-        t = self.bufs.get(key)
-        if t is None or t.numel() < shape or t.dtype != dtype:
+        dev = -1 if pinned else torch.cuda.current_device()
+        ent = self.bufs.get((key, shape, dev))
+        if ent is None or ent[0].dtype != dtype:
             t = (torch.empty(shape, dtype=dtype, pin_memory=True) if pinned
                  else torch.empty(shape, dtype=dtype, device="cuda"))
-            self.bufs[key] = t
-        return t[:shape]
+            ent = (t, t.numpy() if pinned else None, t.data_ptr())
+            self.bufs[(key, shape, dev)] = ent
+        return ent
 
 
 _staging = _HostStaging()
@@ -161,29 +166,44 @@ def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray
     rsr_multiply_host call (H2D + multiply + D2H + sync)."""
     import torch
     raw = np.asarray(v_in)
-    integer_input = raw.dtype.kind in "iub"
-    v = as_vector(v_in)
-    if v.shape[0] != idx.rows:
-        raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
-    if compute is None:
-        compute = "int32" if integer_input and np.abs(v).max(initial=0) < 2 ** 31 else "float64"
-    if compute == "int32":
-        vh = _staging.get("v_i32", idx.rows, torch.int32, True)
-        vh.numpy()[:] = v.astype(np.int32) if not integer_input else raw.astype(np.int32)
-        vcode, dv = _native.I32, _staging.get("dv_i32", idx.rows, torch.int32, False)
-    elif compute == "float64":
-        vh = _staging.get("v_f64", idx.rows, torch.float64, True)
-        vh.numpy()[:] = v
-        vcode, dv = _native.F64, _staging.get("dv_f64", idx.rows, torch.float64, False)
-    else:
-        raise ValueError("compute must be int32 or float64 for host vectors")
+    if raw.dtype.kind in "iub" and compute in (None, "int32"):
+        # integer activations (always finite): no float64 round trip, range check only
+        # for dtypes wider than int32
+        if raw.ndim != 1 or raw.shape[0] < 1:
+            raise ValueError("vector must be 1-D with at least one entry")
+        if raw.shape[0] != idx.rows:
+            raise ValueError(f"vector length {raw.shape[0]} does not match {idx.rows} rows")
+        narrow = raw.dtype.itemsize < 4 or raw.dtype == np.int32
+        if narrow or (raw.min() >= -2 ** 31 and raw.max() < 2 ** 31):
+            vh = _staging.get("v_i32", idx.rows, torch.int32, True)
+            vh[1][:] = raw
+            vcode, dv = _native.I32, _staging.get("dv_i32", idx.rows, torch.int32, False)
+            compute = "int32"
+        elif compute == "int32":
+            raise ValueError("integer activations exceed the int32 range")
+    if compute != "int32" or raw.dtype.kind not in "iub":
+        v = as_vector(v_in)
+        if v.shape[0] != idx.rows:
+            raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
+        if compute == "int32":
+            if np.any(v != np.round(v)) or np.abs(v).max(initial=0) >= 2 ** 31:
+                raise ValueError("compute='int32' needs integer-valued activations in the int32 range")
+            vh = _staging.get("v_i32", idx.rows, torch.int32, True)
+            vh[1][:] = v.astype(np.int32)
+            vcode, dv = _native.I32, _staging.get("dv_i32", idx.rows, torch.int32, False)
+        elif compute in (None, "float64"):
+            vh = _staging.get("v_f64", idx.rows, torch.float64, True)
+            vh[1][:] = v
+            vcode, dv = _native.F64, _staging.get("dv_f64", idx.rows, torch.float64, False)
+        else:
+            raise ValueError("compute must be int32 or float64 for host vectors")
     oh = _staging.get("o_f64", idx.cols, torch.float64, True)
     do = _staging.get("do_f64", idx.cols, torch.float64, False)
     _native.check(_native.lib().rsr_multiply_host(
-        ctypes.byref(idx.desc), vh.data_ptr(), vcode, oh.data_ptr(), _native.F64,
-        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, dv.data_ptr(), do.data_ptr(),
+        ctypes.byref(idx.desc), vh[2], vcode, oh[2], _native.F64,
+        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, dv[2], do[2],
         _native.current_stream_ptr()))
-    return oh.numpy().copy()
+    return oh[1].copy()
 
 
 def _is_device_tensor(v) -> bool:
@@ -245,15 +265,23 @@ def multiply_parallel(v, idx, variant: str = "rsrpp", worker_count: int = 1, *, 
 
 
 def multiply_batched(V, idx, variant: str = "rsrpp"):
-    """V [batch, rows] CUDA tensor -> [batch, cols] (one multiply per row of V)."""
+    """V [batch, rows] CUDA tensor -> [batch, cols] of the same dtype.  int32 / fp32 run the
+    batched gather kernel (csrc/batched.cu: each index byte read once per slice of up to 128
+    vectors); fp64 runs one multiply per vector.  The reference has no batch API: this equals
+    `multiply_ternary` / `multiply_rsr` applied to every row of V (kernels.py:185-206)."""
     import torch
     use_fold = _use_fold(variant)
     if not _is_device_tensor(V) or V.dim() != 2 or V.shape[1] != idx.rows:
         raise ValueError("V must be a CUDA tensor of shape [batch, rows]")
     V = V.contiguous()
-    out = torch.empty((V.shape[0], idx.cols), dtype=V.dtype, device=V.device)
     code = _torch_dtype_code(V)
+    out = torch.empty((V.shape[0], idx.cols), dtype=V.dtype, device=V.device)
+    nbytes = _native.lib().rsr_multiply_batched_workspace_bytes(ctypes.byref(idx.desc), V.shape[0], code)
+    # int64 elements: at least nbytes (allocations are 256-byte aligned)
+    ws = _staging.get("batch_ws", max(1, (nbytes + 7) // 8), torch.int64, False)[0] if nbytes else None
     _native.check(_native.lib().rsr_multiply_batched(
         ctypes.byref(idx.desc), V.data_ptr(), code, V.shape[0], out.data_ptr(), code,
-        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, _native.current_stream_ptr()))
+        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR,
+        ws.data_ptr() if ws is not None else None, ws.numel() * 8 if ws is not None else 0,
+        _native.current_stream_ptr()))
     return out

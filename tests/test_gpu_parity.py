@@ -278,3 +278,39 @@ def test_fp32_fixed_point_scatter_deterministic(rsr, cuda):
         assert _fp32_ok(g, ref)
         auto = rsr.multiply_ternary(dv, tidx).cpu().numpy()
         assert _fp32_ok(auto, ref)
+
+
+@pytest.mark.parametrize("rows,cols,k,batch", [
+    (300, 77, 6, 5), (1000, 333, 2, 33), (4096, 1000, 9, 64), (2000, 130, 1, 1),
+    (16384, 600, 11, 64), (5000, 257, 12, 100), (70000, 40, 8, 3),
+])
+def test_batched_matches_per_vector(rsr, cuda, rows, cols, k, batch):
+    """multiply_batched (csrc/batched.cu, gather form over V^T) == the reference per-vector
+    multiply for every row of V: bitwise for int32 (both variants, ternary and binary), within
+    the fp32 bar for float32; covers short last blocks, k < 3 (warps with empty bucket
+    ranges), batches across the 32/64/128-vector slice widths and u32 perms (rows > 65536)."""
+    import torch
+    rng = np.random.default_rng([rows, cols, k, batch])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+    Vi = rng.integers(-100, 101, size=(batch, rows)).astype(np.int32)
+    kp = c_oracle.keys_ternary(A, k, 1)
+    kn = c_oracle.keys_ternary(A, k, -1)
+    for variant in ("rsrpp", "rsr"):
+        got = rsr.multiply_batched(torch.from_numpy(Vi).cuda(), tidx, variant).cpu().numpy()
+        for i in range(batch):
+            ref = c_oracle.multiply_parallel(Vi[i].astype(np.float64), kp, kn, cols, k, True, 1)
+            assert np.array_equal(got[i].astype(np.float64), ref), (variant, i)
+    Vf = (rng.standard_normal((batch, rows)) * 2).astype(np.float32)
+    gotf = rsr.multiply_batched(torch.from_numpy(Vf).cuda(), tidx).cpu().numpy()
+    again = rsr.multiply_batched(torch.from_numpy(Vf).cuda(), tidx).cpu().numpy()
+    assert gotf.tobytes() == again.tobytes()  # deterministic
+    reff = Vf.astype(np.float64) @ A.astype(np.float64)
+    for i in range(batch):
+        assert _fp32_ok(gotf[i], reff[i]), i
+    # binary index (one half)
+    B = (A == 1).astype(np.uint8)
+    bidx = rsr.preprocess(rsr.BinaryMatrix.from_dense(B), k)
+    gotb = rsr.multiply_batched(torch.from_numpy(Vi).cuda(), bidx).cpu().numpy()
+    refb = Vi.astype(np.int64) @ B.astype(np.int64)
+    assert np.array_equal(gotb.astype(np.int64), refb)

@@ -114,3 +114,24 @@ def test_package_has_no_oracle_dependency():
             if f.endswith((".py", ".cu", ".cuh")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in src.replace("oracle-free", ""), f
+
+
+def test_butterfly_schedule_roundtrip():
+    """indexer.unschedule_codes inverts the device schedule format (csrc/common.cuh butterfly8,
+    control bits 3c..3c+2 in bits 13-15 of code c of each 8-row group): 4096 distinct orders,
+    and scheduling + unscheduling is the identity on row-order codes."""
+    import numpy as np
+    from paper_2411_06360_b200.indexer import _butterfly8, unschedule_codes
+    ctrl = np.arange(4096, dtype=np.uint32)
+    perms = _butterfly8(np.broadcast_to(np.arange(8), (4096, 8)), ctrl)
+    assert len({tuple(p) for p in perms}) == 4096
+    rng = np.random.default_rng(7)
+    nb, rs, k = 3, 512, 11
+    codes = (rng.integers(0, 1 << k, size=(nb, rs)) << 2).astype(np.uint32)   # swizzled key << 2
+    g = codes.reshape(nb, rs // 8, 8)
+    c = rng.integers(0, 4096, size=g.shape[:2]).astype(np.uint32)
+    slots = _butterfly8(g, c)                       # slot s holds row p[s]
+    for j in range(4):
+        slots[..., j] |= ((c >> (3 * j)) & 7) << 13
+    back = unschedule_codes(slots.reshape(nb, rs).astype(np.uint16), k)
+    assert np.array_equal(back, codes.astype(np.uint16))
