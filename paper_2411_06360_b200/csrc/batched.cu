@@ -302,8 +302,7 @@ rsr_status launch_batched_t(const rsr_index_desc& d, const void* V, int64_t batc
   dim3 grid((unsigned)d.nblocks, (unsigned)(ld / sw));
   auto go = [&](auto kern) -> rsr_status {
     if (smem > 48 * 1024) {
-      rsr_status a = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                                "batched smem attribute");
+      rsr_status a = set_max_smem((const void*)kern, smem);
       if (a != RSR_OK) return a;
     }
     kern<<<grid, kBatchWarps * 32, smem, s>>>(p);

@@ -2,6 +2,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -21,6 +24,7 @@ rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t ld
                          void* out, cudaStream_t s);
 rsr_status block_product(const double* u, int w, int use_fold, double* buf, double* out, cudaStream_t s);
 size_t batched_workspace_bytes(const rsr_index_desc& d, int64_t batch, rsr_dtype dt);
+
 rsr_status multiply_batched(const rsr_index_desc& d, const void* V, rsr_dtype vt, int64_t batch, void* out,
                             rsr_dtype ot, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s);
 
@@ -70,6 +74,19 @@ size_t device_max_smem_optin() {
     g_smem_optin[dev] = n;
   }
   return (size_t)g_smem_optin[dev];
+}
+
+rsr_status set_max_smem(const void* kernel, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, kernel}];
+  if (have >= smem) return RSR_OK;
+  rsr_status st = cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                             "max dynamic smem attribute");
+  if (st == RSR_OK) have = smem;
+  return st;
 }
 
 static rsr_status check_k(int64_t rows, int32_t k) {
@@ -168,7 +185,10 @@ rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_d
   bool loop = v_dtype == RSR_F64;
   if (!loop) {
     const size_t index_bytes = (size_t)desc->halves * desc->nblocks * desc->row_stride * 2;
-    loop = index_bytes <= ((size_t)96 << 20) && desc->k <= 14 && out_dtype == v_dtype;
+    // (only where the per-vector AUTO path is the scatter kernel: int32, or fp32 within the
+    // fixed-point limits)
+    const bool scatter = desc->k <= 14 && (v_dtype == RSR_I32 || desc->rows <= 16384);
+    loop = index_bytes <= ((size_t)96 << 20) && scatter && out_dtype == v_dtype;
     if (const char* e = getenv("RSR_B200_BATCH_FORM")) loop = e[0] == 'l';
   }
   if (loop) {  // one multiply per vector

@@ -21,6 +21,8 @@ rsr_status fail(rsr_status st, const std::string& msg);
 rsr_status cuda_check(cudaError_t e, const char* what);
 int device_sm_count();
 size_t device_max_smem_optin();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size)
+rsr_status set_max_smem(const void* kernel, size_t smem);
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

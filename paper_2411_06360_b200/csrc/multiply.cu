@@ -798,8 +798,7 @@ rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int t
                                        : scatter_kernel<kScatterR, PP, true, OutT, FX, false>)
                             : (p.sched ? scatter_kernel<kScatterR, PP, false, OutT, FX, true>
                                        : scatter_kernel<kScatterR, PP, false, OutT, FX, false>);
-  rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                             "scatter smem attribute");
+  rsr_status st = set_max_smem((const void*)kern, smem);
   if (st != RSR_OK) return st;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -915,8 +914,7 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
   const int grid = std::max(1, std::min(nblk, device_sm_count() * per_sm));
   auto kern = d.perm_bytes == 2 ? (pp ? gather_kernel<T, true, true> : gather_kernel<T, false, true>)
                                 : (pp ? gather_kernel<T, true, false> : gather_kernel<T, false, false>);
-  rsr_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                             "gather smem attribute");
+  rsr_status st = set_max_smem((const void*)kern, smem);
   if (st != RSR_OK) return st;
   kern<<<grid, kGatherWarps * 32, smem, s>>>(p);
   return cuda_check(cudaGetLastError(), "gather_kernel launch");

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -125,6 +126,7 @@ class _HostStaging(threading.local):
 
     def __init__(self):
         self.bufs = {}
+        self.plans = {}  # id(index) -> (weakref to the index, {kind: _HostPlan}); no strong refs
 
     def get(self, key, shape, dtype, pinned):
         """(tensor, numpy view or None, data pointer) of a cached buffer of `shape` elements."""
@@ -140,6 +142,47 @@ class _HostStaging(threading.local):
 
 
 _staging = _HostStaging()
+
+
+class _HostPlan:
+    """Everything one host-buffer multiply against one index needs, resolved once per thread:
+    pinned staging views, device scratch pointers, the descriptor reference."""
+    __slots__ = ("v_np", "args_v", "o_np", "args_o", "desc_ref", "fn")
+
+    def __init__(self, idx, kind):
+        import torch
+        tdt = {"i32": torch.int32, "f64": torch.float64}[kind]
+        vh = _staging.get("v_" + kind, idx.rows, tdt, True)
+        dv = _staging.get("dv_" + kind, idx.rows, tdt, False)
+        oh = _staging.get("o_f64", idx.cols, torch.float64, True)
+        do = _staging.get("do_f64", idx.cols, torch.float64, False)
+        self.v_np, self.o_np = vh[1], oh[1]
+        self.args_v = (ctypes.c_void_p(vh[2]), {"i32": _native.I32, "f64": _native.F64}[kind])
+        self.args_o = (ctypes.c_void_p(oh[2]), _native.F64)
+        self.desc_ref = ctypes.byref(idx.desc)
+        self.fn = (_native.lib().rsr_multiply_host, ctypes.c_void_p(dv[2]), ctypes.c_void_p(do[2]))
+
+
+def _host_plan(idx, kind) -> _HostPlan:
+    plans = _staging.plans
+    ent = plans.get(id(idx))
+    if ent is None or ent[0]() is not idx:
+        key = id(idx)
+        ent = plans[key] = (weakref.ref(idx, lambda _r, k=key, d=plans: d.pop(k, None)), {})
+    per = ent[1]
+    plan = per.get(kind)
+    if plan is None:
+        plan = per[kind] = _HostPlan(idx, kind)
+    return plan
+
+
+def _run_host_plan(plan: _HostPlan, use_fold: bool) -> np.ndarray:
+    fn, dv, do = plan.fn
+    st = fn(plan.desc_ref, plan.args_v[0], plan.args_v[1], plan.args_o[0], plan.args_o[1],
+            _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, dv, do, _native.current_stream_ptr())
+    if st:
+        _native.check(st)
+    return plan.o_np.copy()
 
 
 def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO):
@@ -162,9 +205,8 @@ def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_n
 
 
 def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray:
-    """Host-buffer path (reference contract): NumPy in, fp64 NumPy out, via one
+    """Host-buffer path (reference contract): NumPy in, fresh fp64 NumPy out, via one
     rsr_multiply_host call (H2D + multiply + D2H + sync)."""
-    import torch
     raw = np.asarray(v_in)
     if raw.dtype.kind in "iub" and compute in (None, "int32"):
         # integer activations (always finite): no float64 round trip, range check only
@@ -173,37 +215,26 @@ def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray
             raise ValueError("vector must be 1-D with at least one entry")
         if raw.shape[0] != idx.rows:
             raise ValueError(f"vector length {raw.shape[0]} does not match {idx.rows} rows")
-        narrow = raw.dtype.itemsize < 4 or raw.dtype == np.int32
-        if narrow or (raw.min() >= -2 ** 31 and raw.max() < 2 ** 31):
-            vh = _staging.get("v_i32", idx.rows, torch.int32, True)
-            vh[1][:] = raw
-            vcode, dv = _native.I32, _staging.get("dv_i32", idx.rows, torch.int32, False)
-            compute = "int32"
-        elif compute == "int32":
-            raise ValueError("integer activations exceed the int32 range")
-    if compute != "int32" or raw.dtype.kind not in "iub":
-        v = as_vector(v_in)
-        if v.shape[0] != idx.rows:
-            raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
+        if raw.dtype.itemsize < 4 or raw.dtype == np.int32 or (raw.min() >= -2 ** 31 and raw.max() < 2 ** 31):
+            plan = _host_plan(idx, "i32")
+            plan.v_np[:] = raw
+            return _run_host_plan(plan, use_fold)
         if compute == "int32":
-            if np.any(v != np.round(v)) or np.abs(v).max(initial=0) >= 2 ** 31:
-                raise ValueError("compute='int32' needs integer-valued activations in the int32 range")
-            vh = _staging.get("v_i32", idx.rows, torch.int32, True)
-            vh[1][:] = v.astype(np.int32)
-            vcode, dv = _native.I32, _staging.get("dv_i32", idx.rows, torch.int32, False)
-        elif compute in (None, "float64"):
-            vh = _staging.get("v_f64", idx.rows, torch.float64, True)
-            vh[1][:] = v
-            vcode, dv = _native.F64, _staging.get("dv_f64", idx.rows, torch.float64, False)
-        else:
-            raise ValueError("compute must be int32 or float64 for host vectors")
-    oh = _staging.get("o_f64", idx.cols, torch.float64, True)
-    do = _staging.get("do_f64", idx.cols, torch.float64, False)
-    _native.check(_native.lib().rsr_multiply_host(
-        ctypes.byref(idx.desc), vh[2], vcode, oh[2], _native.F64,
-        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, dv[2], do[2],
-        _native.current_stream_ptr()))
-    return oh[1].copy()
+            raise ValueError("integer activations exceed the int32 range")
+    v = as_vector(v_in)
+    if v.shape[0] != idx.rows:
+        raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
+    if compute == "int32":
+        if np.any(v != np.round(v)) or np.abs(v).max(initial=0) >= 2 ** 31:
+            raise ValueError("compute='int32' needs integer-valued activations in the int32 range")
+        plan = _host_plan(idx, "i32")
+        plan.v_np[:] = v.astype(np.int32)
+    elif compute in (None, "float64"):
+        plan = _host_plan(idx, "f64")
+        plan.v_np[:] = v
+    else:
+        raise ValueError("compute must be int32 or float64 for host vectors")
+    return _run_host_plan(plan, use_fold)
 
 
 def _is_device_tensor(v) -> bool:
