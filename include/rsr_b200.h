@@ -111,6 +111,21 @@ rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_d
                         rsr_dtype out_dtype, rsr_variant variant, rsr_form form,
                         int32_t block_begin, int32_t block_end, void* stream);
 
+/* Replaces `load_index` -> RsrIndex.from_blocks (store.py:49-101, indexer.py:89-129): import
+ * a stored index whose per-block arrays are already on the device — d_perm{0,1}: u32
+ * [nblocks][rows] stable row orders, d_seg{0,1}: u32 [nblocks][seg_stride] segment starts
+ * (2^w used per block, no sentinel), half 1 only for a ternary desc.  Validates the
+ * invariants on the device (d_error[0] |= 1 perm out of range, 2 perm not a bijection,
+ * 4 segmentation does not start at 0, 8 segmentation decreasing or > rows; d_error[1] =
+ * lowest failing block; the caller initializes d_error to {0, INT32_MAX} and reads it after
+ * the stream), writes the device layout of `desc` (arrays from rsr_index_layout) including
+ * the key codes rebuilt from the segments, and schedules the keys.  `workspace` needs
+ * rsr_index_import_workspace_bytes(desc) device bytes. */
+size_t rsr_index_import_workspace_bytes(const rsr_index_desc* desc);
+rsr_status rsr_index_import(const rsr_index_desc* desc, const uint32_t* d_perm0, const uint32_t* d_seg0,
+                            const uint32_t* d_perm1, const uint32_t* d_seg1, int64_t seg_stride,
+                            void* workspace, size_t workspace_bytes, int32_t* d_error, void* stream);
+
 /* Batched multiply: V [batch][rows] -> OUT [batch][cols] on the current stream, every index
  * byte read once per slice of up to 128 vectors instead of once per vector (SURVEY.md §8(d)
  * config 3; the reference has no batch API and runs `multiply_ternary`, kernels.py:196-206,

@@ -24,6 +24,7 @@ ABI_VERSION = 2
 EXPORTS = (
     "rsr_b200_abi_version", "rsr_b200_last_error", "rsr_index_layout",
     "rsr_preprocess_workspace_bytes", "rsr_preprocess_ternary", "rsr_preprocess_binary",
+    "rsr_index_import_workspace_bytes", "rsr_index_import",
     "rsr_multiply", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host", "rsr_segmented_sum",
     "rsr_block_product", "rsr_naive_multiply_ternary",
 )
@@ -75,6 +76,10 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, I32_, I32_, P]
     L.rsr_multiply.restype = st
+    L.rsr_index_import_workspace_bytes.argtypes = [ctypes.POINTER(IndexDesc)]
+    L.rsr_index_import_workspace_bytes.restype = SZ
+    L.rsr_index_import.argtypes = [ctypes.POINTER(IndexDesc), P, P, P, P, I64, P, SZ, P, P]
+    L.rsr_index_import.restype = st
     L.rsr_multiply_batched_workspace_bytes.argtypes = [ctypes.POINTER(IndexDesc), I64, ctypes.c_int]
     L.rsr_multiply_batched_workspace_bytes.restype = SZ
     L.rsr_multiply_batched.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, I64, P,

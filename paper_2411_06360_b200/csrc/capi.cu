@@ -24,6 +24,10 @@ rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t ld
                          void* out, cudaStream_t s);
 rsr_status block_product(const double* u, int w, int use_fold, double* buf, double* out, cudaStream_t s);
 size_t batched_workspace_bytes(const rsr_index_desc& d, int64_t batch, rsr_dtype dt);
+size_t index_import_workspace_bytes(const rsr_index_desc* d);
+rsr_status index_import(const rsr_index_desc* d, const uint32_t* perm0, const uint32_t* seg0, const uint32_t* perm1,
+                        const uint32_t* seg1, int64_t seg_in_stride, void* ws, size_t ws_bytes, int32_t* err,
+                        cudaStream_t s);
 
 rsr_status multiply_batched(const rsr_index_desc& d, const void* V, rsr_dtype vt, int64_t batch, void* out,
                             rsr_dtype ot, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s);
@@ -154,6 +158,15 @@ rsr_status rsr_preprocess_ternary(const int8_t* A, int64_t lda, const rsr_index_
 rsr_status rsr_preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_desc* desc, void* workspace,
                                  size_t workspace_bytes, void* stream) {
   return preprocess_binary(bits, ldb, desc, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t rsr_index_import_workspace_bytes(const rsr_index_desc* desc) { return index_import_workspace_bytes(desc); }
+
+rsr_status rsr_index_import(const rsr_index_desc* desc, const uint32_t* d_perm0, const uint32_t* d_seg0,
+                            const uint32_t* d_perm1, const uint32_t* d_seg1, int64_t seg_stride, void* workspace,
+                            size_t workspace_bytes, int32_t* d_error, void* stream) {
+  return index_import(desc, d_perm0, d_seg0, d_perm1, d_seg1, seg_stride, workspace, workspace_bytes, d_error,
+                      (cudaStream_t)stream);
 }
 
 rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_dtype, void* out, rsr_dtype out_dtype,

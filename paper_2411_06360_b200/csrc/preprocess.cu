@@ -304,6 +304,65 @@ rsr_status launch_schedule(const rsr_index_desc& d, cudaStream_t s) {
   return cuda_check(cudaGetLastError(), "schedule_keys_kernel launch");
 }
 
+// ---------------------------------------------------------------------------------------
+// Import of a stored index (`.rsx`, store.py:49-101): per block a u32 permutation and 2^w
+// u32 segment starts.  One warp per (half, block) validates the invariants the reference's
+// RsrIndex.from_blocks checks (indexer.py:89-129) — permutation a bijection (a seen-bitmap
+// with atomicOr), segmentation starting at 0, non-decreasing, <= rows — writes our layout
+// (u16/u32 perm, u32 seg + sentinel) and rebuilds every row's key code from the segments on
+// the device (lane j walks bucket j), replacing the host-side `_buckets_from_segments`
+// (indexer.py:176-186).  err[0] |= flags, err[1] = min failing block.
+enum : int { kImpPermRange = 1, kImpPermDup = 2, kImpSeg0 = 4, kImpSegOrder = 8 };
+
+__global__ void import_blocks_kernel(rsr_index_desc d, int h, const uint32_t* __restrict__ perm_in,
+                                     const uint32_t* __restrict__ seg_in, int64_t seg_in_stride,
+                                     uint32_t* __restrict__ seen, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= d.nblocks) return;
+  const int w = block_width(d.cols, d.k, b);
+  const int nbk = 1 << w;
+  const int64_t rows = d.rows;
+  const uint32_t* pin = perm_in + (int64_t)b * rows;
+  const uint32_t* sin = seg_in + (int64_t)b * seg_in_stride;
+  uint32_t* seg = d.half[h].seg + (int64_t)b * d.seg_stride;
+  uint16_t* key = d.half[h].bucket + (int64_t)b * d.row_stride;
+  uint32_t* my_seen = seen + (int64_t)b * ((rows + 31) / 32);
+  int flags = 0;
+  for (int j = lane; j < nbk; j += 32) {
+    const uint32_t sj = sin[j];
+    if (j == 0 && sj != 0) flags |= kImpSeg0;
+    if ((j > 0 && sin[j - 1] > sj) || sj > (uint64_t)rows) flags |= kImpSegOrder;
+    seg[j] = sj;
+  }
+  for (int64_t j = nbk + lane; j < d.seg_stride; j += 32) seg[j] = (uint32_t)rows;  // sentinel (+ unused tail)
+  for (int64_t p = lane; p < rows; p += 32) {
+    const uint32_t r = pin[p];
+    if (r >= rows) {
+      flags |= kImpPermRange;
+      continue;
+    }
+    if (d.perm_bytes == 2) reinterpret_cast<uint16_t*>(d.half[h].perm)[(int64_t)b * d.row_stride + p] = (uint16_t)r;
+    else reinterpret_cast<uint32_t*>(d.half[h].perm)[(int64_t)b * d.row_stride + p] = r;
+    const uint32_t bit = 1u << (r & 31);
+    if (atomicOr(&my_seen[r >> 5], bit) & bit) flags |= kImpPermDup;
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (flags) {  // do not walk a broken segmentation
+    if (lane == 0) {
+      atomicOr(&err[0], flags);
+      atomicMin(&err[1], b);
+    }
+    return;
+  }
+  // key codes: rows of bucket j are pin[sin[j] .. sin[j+1])
+  for (int j = lane; j < nbk; j += 32) {
+    const uint32_t e = j + 1 < nbk ? sin[j + 1] : (uint32_t)rows;
+    const uint16_t code = (uint16_t)encode_key((uint32_t)j, d.k);
+    for (uint32_t q = sin[j]; q < e; ++q) key[pin[q]] = code;
+  }
+}
+
 rsr_status clear_index(const rsr_index_desc& d, cudaStream_t s) {
   for (int h = 0; h < d.halves; ++h) {
     size_t nb = (size_t)d.nblocks * d.row_stride;
@@ -361,6 +420,33 @@ rsr_status preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_d
                                           d->half[0].bucket);
   if ((st = cuda_check(cudaGetLastError(), "keys_binary_kernel launch")) != RSR_OK) return st;
   if ((st = launch_sort(*d, ws, ws_bytes, s)) != RSR_OK) return st;
+  return launch_schedule(*d, s);
+}
+
+size_t index_import_workspace_bytes(const rsr_index_desc* d) {
+  return d ? (size_t)d->halves * d->nblocks * (size_t)((d->rows + 31) / 32) * 4 : 0;
+}
+
+rsr_status index_import(const rsr_index_desc* d, const uint32_t* perm0, const uint32_t* seg0, const uint32_t* perm1,
+                        const uint32_t* seg1, int64_t seg_in_stride, void* ws, size_t ws_bytes, int32_t* err,
+                        cudaStream_t s) {
+  rsr_status st = check_desc(d);
+  if (st != RSR_OK) return st;
+  if (!perm0 || !seg0 || (d->halves == 2 && (!perm1 || !seg1)) || !err)
+    return fail(RSR_ERR_INVALID, "null import arrays");
+  if (seg_in_stride < ((int64_t)1 << d->k)) return fail(RSR_ERR_INVALID, "segment stride must be >= 2^k");
+  if (!ws || ws_bytes < index_import_workspace_bytes(d)) return fail(RSR_ERR_INVALID, "import workspace too small");
+  if ((st = clear_index(*d, s)) != RSR_OK) return st;
+  if ((st = cuda_check(cudaMemsetAsync(ws, 0, index_import_workspace_bytes(d), s), "memset import bitmap")) != RSR_OK)
+    return st;
+  const int wpc = 8;
+  const unsigned grid = (unsigned)((d->nblocks + wpc - 1) / wpc);
+  const size_t half_words = (size_t)d->nblocks * ((d->rows + 31) / 32);
+  for (int h = 0; h < d->halves; ++h) {
+    import_blocks_kernel<<<grid, 32 * wpc, 0, s>>>(*d, h, h ? perm1 : perm0, h ? seg1 : seg0, seg_in_stride,
+                                                    (uint32_t*)ws + h * half_words, err);
+    if ((st = cuda_check(cudaGetLastError(), "import_blocks_kernel launch")) != RSR_OK) return st;
+  }
   return launch_schedule(*d, s);
 }
 

@@ -133,12 +133,71 @@ def tuner() -> dict:
             "max_k": np.array([rsr.max_k_for_rows(int(n)) for n in ns], np.int64)}
 
 
+def rsx_files() -> dict:
+    """.rsx files written by the reference's save_index (store.py:31-45) and the reference's
+    load_index verdict on corrupted copies (store.py:48-101): valid files carry the product
+    of a fixed vector, corrupt ones the exact FormatError message."""
+    import json
+    import struct
+    from rsr import store
+    out = {}
+    rsx_dir = os.path.join(HERE, "rsx")
+    os.makedirs(rsx_dir, exist_ok=True)
+    rng = np.random.default_rng(2024)
+    A = rng.integers(-1, 2, size=(200, 77), dtype=np.int8)
+    tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), 5)
+    B = (rng.integers(0, 2, size=(90, 33))).astype(np.uint8)
+    bidx = rsr.preprocess(rsr.BinaryMatrix.from_dense(B), 4)
+    vt = rng.integers(-50, 51, size=200).astype(np.float64)
+    vb = rng.integers(-50, 51, size=90).astype(np.float64)
+    store.save_index(tidx, os.path.join(rsx_dir, "ternary_200x77_k5.rsx"))
+    store.save_index(bidx, os.path.join(rsx_dir, "binary_90x33_k4.rsx"))
+    out["ternary_v"] = vt
+    out["ternary_y"] = rsr.multiply_ternary(vt, tidx)
+    out["binary_v"] = vb
+    out["binary_y"] = rsr.multiply_rsr(vb, bidx)
+    good = open(os.path.join(rsx_dir, "binary_90x33_k4.rsx"), "rb").read()
+    hdr = store.HEADER_BYTES
+    first_perm = hdr + 2                       # block 0: u16 width, then perm u32 [rows]
+    first_seg = first_perm + 4 * 90
+    def put_u32(raw, off, val):
+        raw = bytearray(raw)
+        struct.pack_into("<I", raw, off, val)
+        return bytes(raw)
+    corrupt = {
+        "bad_magic": b"RSX9" + good[4:],
+        "bad_version": good[:4] + struct.pack("<H", 7) + good[6:],
+        "bad_kind": good[:6] + bytes([5]) + good[7:],
+        "truncated_header": good[:20],
+        "truncated_payload": good[:-5],
+        "trailing_bytes": good + b"\x00",
+        "bad_block_count": good[:25] + struct.pack("<I", 3) + good[29:],
+        "bad_width": good[:hdr] + struct.pack("<H", 3) + good[hdr + 2:],
+        "perm_duplicate": put_u32(good, first_perm + 4, struct.unpack_from("<I", good, first_perm)[0]),
+        "perm_range": put_u32(good, first_perm, 90),
+        "seg_start": put_u32(good, first_seg, 1),
+        "seg_order": put_u32(good, first_seg + 4 * 3, 0),
+    }
+    verdicts = {}
+    for name, raw in corrupt.items():
+        path = os.path.join(rsx_dir, f"corrupt_{name}.rsx")
+        open(path, "wb").write(raw)
+        try:
+            store.load_index(path)
+            verdicts[name] = None
+        except rsr.FormatError as exc:
+            verdicts[name] = str(exc)
+    json.dump(verdicts, open(os.path.join(rsx_dir, "verdicts.json"), "w"), indent=1, sort_keys=True)
+    return out
+
+
 def main() -> None:
     np.savez_compressed(os.path.join(HERE, "worked_example.npz"), **worked_example())
     np.savez_compressed(os.path.join(HERE, "fuzz_small.npz"), **fuzz_cases(101, 60, 64, 8))
     np.savez_compressed(os.path.join(HERE, "medium.npz"), **medium_cases())
     np.savez_compressed(os.path.join(HERE, "folds.npz"), **folds())
     np.savez_compressed(os.path.join(HERE, "tuner.npz"), **tuner())
+    np.savez_compressed(os.path.join(HERE, "rsx_products.npz"), **rsx_files())
     print("reference rsr", rsr.__version__, "golden vectors written to", HERE)
 
 

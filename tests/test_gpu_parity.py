@@ -314,3 +314,45 @@ def test_batched_matches_per_vector(rsr, cuda, rows, cols, k, batch):
     gotb = rsr.multiply_batched(torch.from_numpy(Vi).cuda(), bidx).cpu().numpy()
     refb = Vi.astype(np.int64) @ B.astype(np.int64)
     assert np.array_equal(gotb.astype(np.int64), refb)
+
+
+def test_rsx_load_golden(rsr, cuda):
+    """Reference-written .rsx files load into the device layout and multiply to the
+    reference's products; invariant corruptions raise the reference's messages; our writer
+    reproduces the reference's file byte for byte from a GPU-preprocessed index."""
+    import json
+    import os
+    import torch
+    rsx = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "rsx")
+    prods = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "rsx_products.npz"))
+    tidx = rsr.load_index(os.path.join(rsx, "ternary_200x77_k5.rsx"))
+    bidx = rsr.load_index(os.path.join(rsx, "binary_90x33_k4.rsx"))
+    assert isinstance(tidx, rsr.TernaryIndex) and isinstance(bidx, rsr.RsrIndex)
+    assert np.array_equal(rsr.multiply_ternary(prods["ternary_v"], tidx), prods["ternary_y"])
+    assert np.array_equal(rsr.multiply_rsr(prods["binary_v"], bidx), prods["binary_y"])
+    # device int32 path too (scheduled keys rebuilt on the device)
+    got = rsr.multiply_ternary(torch.from_numpy(prods["ternary_v"].astype(np.int32)).cuda(), tidx)
+    assert np.array_equal(got.cpu().numpy().astype(np.float64), prods["ternary_y"])
+    verdicts = json.load(open(os.path.join(rsx, "verdicts.json")))
+    for name in ("perm_duplicate", "perm_range", "seg_start", "seg_order"):
+        with pytest.raises(rsr.FormatError) as exc:
+            rsr.load_index(os.path.join(rsx, f"corrupt_{name}.rsx"))
+        assert str(exc.value) == verdicts[name], name
+    # same matrices as tests/golden/make_golden.py rsx_files(): our preprocess + save == reference file
+    rng = np.random.default_rng(2024)
+    A = rng.integers(-1, 2, size=(200, 77), dtype=np.int8)
+    B = rng.integers(0, 2, size=(90, 33)).astype(np.uint8)
+    import tempfile
+    with tempfile.TemporaryDirectory() as tmp:
+        rsr.save_index(rsr.preprocess_ternary(rsr.TernaryMatrix(A), 5), os.path.join(tmp, "t.rsx"))
+        rsr.save_index(rsr.preprocess(rsr.BinaryMatrix.from_dense(B), 4), os.path.join(tmp, "b.rsx"))
+        assert open(os.path.join(tmp, "t.rsx"), "rb").read() == open(os.path.join(rsx, "ternary_200x77_k5.rsx"), "rb").read()
+        assert open(os.path.join(tmp, "b.rsx"), "rb").read() == open(os.path.join(rsx, "binary_90x33_k4.rsx"), "rb").read()
+        # round trip at a size with u16 perms, scheduled keys and a short last block
+        A2 = np.random.default_rng(5).integers(-1, 2, size=(4096, 1000), dtype=np.int8)
+        i2 = rsr.preprocess_ternary(torch.from_numpy(A2).cuda(), 9)
+        rsr.save_index(i2, os.path.join(tmp, "r.rsx"))
+        back = rsr.load_index(os.path.join(tmp, "r.rsx"))
+        v2 = torch.from_numpy(np.random.default_rng(6).integers(-100, 101, 4096).astype(np.int32)).cuda()
+        assert torch.equal(rsr.multiply_ternary(v2, back), rsr.multiply_ternary(v2, i2))
+        assert all(np.array_equal(a, b) for a, b in zip(back.positive.host_arrays(), i2.positive.host_arrays()))
