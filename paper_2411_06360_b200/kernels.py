@@ -151,14 +151,15 @@ class _HostPlan:
 
     def __init__(self, idx, kind):
         import torch
-        tdt = {"i32": torch.int32, "f64": torch.float64}[kind]
+        tdt = {"i32": torch.int32, "f32": torch.float32, "f64": torch.float64}[kind]
+        odt = torch.float32 if kind == "f32" else torch.float64  # fp32 activations -> fp32 results
         vh = _staging.get("v_" + kind, idx.rows, tdt, True)
         dv = _staging.get("dv_" + kind, idx.rows, tdt, False)
-        oh = _staging.get("o_f64", idx.cols, torch.float64, True)
-        do = _staging.get("do_f64", idx.cols, torch.float64, False)
+        oh = _staging.get("o_" + str(odt), idx.cols, odt, True)
+        do = _staging.get("do_" + str(odt), idx.cols, odt, False)
         self.v_np, self.o_np = vh[1], oh[1]
-        self.args_v = (ctypes.c_void_p(vh[2]), {"i32": _native.I32, "f64": _native.F64}[kind])
-        self.args_o = (ctypes.c_void_p(oh[2]), _native.F64)
+        self.args_v = (ctypes.c_void_p(vh[2]), {"i32": _native.I32, "f32": _native.F32, "f64": _native.F64}[kind])
+        self.args_o = (ctypes.c_void_p(oh[2]), _native.F32 if kind == "f32" else _native.F64)
         self.desc_ref = ctypes.byref(idx.desc)
         self.fn = (_native.lib().rsr_multiply_host, ctypes.c_void_p(dv[2]), ctypes.c_void_p(do[2]))
 
@@ -182,7 +183,7 @@ def _run_host_plan(plan: _HostPlan, use_fold: bool) -> np.ndarray:
             _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, dv, do, _native.current_stream_ptr())
     if st:
         _native.check(st)
-    return plan.o_np.copy()
+    return plan.o_np.astype(np.float64)  # fresh array (fp64, the reference's result type)
 
 
 def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO):
@@ -221,9 +222,25 @@ def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray
             return _run_host_plan(plan, use_fold)
         if compute == "int32":
             raise ValueError("integer activations exceed the int32 range")
+    if raw.dtype == np.float32 and compute in (None, "float32"):
+        # fp32 activations are computed in fp32 (north star: within 1e-5 relative of the
+        # fp64 reference); results come back as fresh fp64 arrays like the reference's
+        if raw.ndim != 1 or raw.shape[0] < 1:
+            raise ValueError("vector must be 1-D with at least one entry")
+        if not np.isfinite(raw).all():
+            raise ValueError("vector entries must be finite")
+        if raw.shape[0] != idx.rows:
+            raise ValueError(f"vector length {raw.shape[0]} does not match {idx.rows} rows")
+        plan = _host_plan(idx, "f32")
+        plan.v_np[:] = raw
+        return _run_host_plan(plan, use_fold)
     v = as_vector(v_in)
     if v.shape[0] != idx.rows:
         raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
+    if compute == "float32":
+        plan = _host_plan(idx, "f32")
+        plan.v_np[:] = v.astype(np.float32)
+        return _run_host_plan(plan, use_fold)
     if compute == "int32":
         if np.any(v != np.round(v)) or np.abs(v).max(initial=0) >= 2 ** 31:
             raise ValueError("compute='int32' needs integer-valued activations in the int32 range")
@@ -233,7 +250,7 @@ def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray
         plan = _host_plan(idx, "f64")
         plan.v_np[:] = v
     else:
-        raise ValueError("compute must be int32 or float64 for host vectors")
+        raise ValueError("compute must be int32, float32 or float64 for host vectors")
     return _run_host_plan(plan, use_fold)
 
 
