@@ -356,3 +356,35 @@ def test_rsx_load_golden(rsr, cuda):
         v2 = torch.from_numpy(np.random.default_rng(6).integers(-100, 101, 4096).astype(np.int32)).cuda()
         assert torch.equal(rsr.multiply_ternary(v2, back), rsr.multiply_ternary(v2, i2))
         assert all(np.array_equal(a, b) for a, b in zip(back.positive.host_arrays(), i2.positive.host_arrays()))
+
+
+def test_bitlinear_decode_chain_graph(rsr, cuda):
+    """BitLinear layers on the Llama-3-8B MLP shapes (up 4096->14336, down 14336->4096) chained
+    on the device and captured in one CUDA graph: fp32 within the north-star tolerance of a
+    dense fp64 reference, int32 bit-exact; graph replay reproduces eager results."""
+    import torch
+    rng = np.random.default_rng(11)
+    Wu = rng.integers(-1, 2, size=(4096, 14336), dtype=np.int8)
+    Wd = rng.integers(-1, 2, size=(14336, 4096), dtype=np.int8)
+    up = rsr.BitLinear(torch.from_numpy(Wu).cuda())
+    down = rsr.BitLinear(torch.from_numpy(Wd).cuda())
+    assert (up.k, down.k) == (rsr.optimal_k_rsrpp(4096), rsr.optimal_k_rsrpp(14336))
+    x = torch.from_numpy(rng.standard_normal(4096).astype(np.float32)).cuda()
+    y = down(up(x) * 0.01)
+    h = (x.cpu().double().numpy() @ Wu.astype(np.float64)).astype(np.float32).astype(np.float64) * 0.01
+    ref = h.astype(np.float32).astype(np.float64) @ Wd.astype(np.float64)
+    assert _fp32_ok(y.cpu().numpy(), ref), float(np.abs(y.cpu().numpy() - ref).max())
+    xi = torch.from_numpy(rng.integers(-8, 9, 4096).astype(np.int32)).cuda()
+    yi = down(up(xi) // 64)
+    hi = (xi.cpu().numpy().astype(np.int64) @ Wu.astype(np.int64)) // 64
+    assert np.array_equal(yi.cpu().numpy().astype(np.int64), hi @ Wd.astype(np.int64))
+    # capture the chain in one graph
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+        yg = down(up(x) * 0.01)
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(yg, y)
