@@ -303,44 +303,48 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         }
       }
     };
-    for (int u = 0; u < nunits; ++u) {
-      if (u + 1 == nunits) grid_launch_dependents();  // the next grid may start its prologue on freed SMs
-      const int hb = u % NH;
-      if (lane == 0 && wbytes && u + 1 + S < nunits) prefetch_unit(u + 1 + S);
-      const uint32_t Hs = hist_s + (uint32_t)(hb * LIMBS * nbk) * 4u;
-      if (warp == 0 && u < 40) TRACE(8 + u * 8 + 0);
-      if (u >= NH) mbar_wait(&hfree[hb], (uint32_t)(((u / NH) - 1) & 1));
-      if (warp == 0 && u < 40) TRACE(8 + u * 8 + 1);
-      const bool more = u + 1 < nunits;
-      kb0 += ustride;
-      if constexpr (TERNARY) kb1 += ustride;
+    // one unit's groups: the reductions of group g, then the next unit's keys of group g (a
+    // whole unit ahead, into the registers just consumed)
+    auto unit_groups = [&](uint32_t Hs, bool more, auto skip0) {
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
-        const uint4 a0 = q0[g];
-        const uint4 a1 = q1[g];
-        if (more && ((gmask >> g) & 1u)) {  // the next unit's keys of this group: a whole unit ahead
-          q0[g] = ld_nc_v4(kb0 + 256 * g);
-          if constexpr (TERNARY) q1[g] = ld_nc_v4(kb1 + 256 * g);
-        }
         // slot s of the group holds row p[s], p = butterfly of the control bits (k <= 11):
         // route the v registers the same way, once for both halves
         int32_t vp[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) vp[e] = vr[g * 8 + e];
-        if constexpr (SCHED) butterfly8(vp, sched_ctrl(a0.x, a0.y));
-        if (warp_all_valid) {
-          reduce_group(Hs, a0, vp, false, std::false_type{});
-          if constexpr (TERNARY) reduce_group(Hs, a1, vp, true, std::false_type{});
-        } else {
-          reduce_group(Hs, a0, vp, false, std::true_type{});
-          if constexpr (TERNARY) reduce_group(Hs, a1, vp, true, std::true_type{});
+        if constexpr (SCHED) butterfly8(vp, sched_ctrl(q0[g].x, q0[g].y));
+        reduce_group(Hs, q0[g], vp, false, skip0);
+        if constexpr (TERNARY) reduce_group(Hs, q1[g], vp, true, skip0);
+        if (more && ((gmask >> g) & 1u)) {
+          q0[g] = ld_nc_v4(kb0 + 256 * g);
+          if constexpr (TERNARY) q1[g] = ld_nc_v4(kb1 + 256 * g);
         }
       }
+    };
+    int hb = 0;            // histogram buffer of unit u (u % NH, kept incrementally)
+    uint32_t hpar = 1;     // parity of hfree[hb]'s phase to wait for: ((u / NH) - 1) & 1
+    for (int u = 0; u < nunits; ++u) {
+      if (u + 1 == nunits) grid_launch_dependents();  // the next grid may start its prologue on freed SMs
+      if (lane == 0 && wbytes && u + 1 + S < nunits) prefetch_unit(u + 1 + S);
+      const uint32_t Hs = hist_s + (uint32_t)(hb * LIMBS * nbk) * 4u;
+      if (warp == 0 && u < 40) TRACE(8 + u * 8 + 0);
+      if (u >= NH) mbar_wait(&hfree[hb], hpar);
+      if (warp == 0 && u < 40) TRACE(8 + u * 8 + 1);
+      const bool more = u + 1 < nunits;
+      kb0 += ustride;
+      if constexpr (TERNARY) kb1 += ustride;
+      if (warp_all_valid) unit_groups(Hs, more, std::false_type{});
+      else unit_groups(Hs, more, std::true_type{});
       __syncwarp();
       if (warp == 0 && u < 40) TRACE(8 + u * 8 + 2);
       if (lane == 0) {
         mbar_arrive(&hfull[hb]);  // release: this warp's reductions are visible to the fold warps
         if (warp == 0 && u < 40) TRACE(8 + u * 8 + 7);
+      }
+      if (++hb == NH) {
+        hb = 0;
+        hpar ^= 1u;
       }
     }
   } else {
@@ -440,11 +444,12 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       if (lane == 14) r = (fw & 2) ? W : 0;
       return r;
     };
-    for (int f = 0; f < nunits; ++f) {
-      const int fb = f % NH;
+    int fb = 0;          // f % NH, kept incrementally
+    uint32_t fpar = 0;   // (f / NH) & 1
+    for (int f = 0; f < nunits; ++f, (++fb == NH ? (fb = 0, fpar ^= 1u) : 0u)) {
       const int32_t* H = hist + fb * LIMBS * nbk;
       if (fw == 0 && f < 40) TRACE(8 + f * 8 + 3);
-      mbar_wait(&hfull[fb], (uint32_t)((f / NH) & 1));
+      mbar_wait(&hfull[fb], fpar);
       if (fw == 0 && f < 40) TRACE(8 + f * 8 + 4);
       int32_t d[LIMBS];  // this block's slot value per limb: fold(H now) - fold(H after block f - NH)
 #pragma unroll
