@@ -316,10 +316,12 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         if constexpr (SCHED) butterfly8(vp, sched_ctrl(q0[g].x, q0[g].y));
         reduce_group(Hs, q0[g], vp, false, skip0);
         if constexpr (TERNARY) reduce_group(Hs, q1[g], vp, true, skip0);
-        if (more && ((gmask >> g) & 1u)) {
-          q0[g] = ld_nc_v4(kb0 + 256 * g);
-          if constexpr (TERNARY) q1[g] = ld_nc_v4(kb1 + 256 * g);
-        }
+        // branch-free (a shared guard lets the compiler merge the four loads and sink them to
+        // the end of the unit, which leaves them no time): without a next unit, or for a group
+        // past the key rows (its rows carry v = 0 and are skipped), load the array base instead
+        const bool ld = more && ((gmask >> g) & 1u);
+        q0[g] = ld_nc_v4(ld ? kb0 + 256 * g : key0);
+        if constexpr (TERNARY) q1[g] = ld_nc_v4(ld ? kb1 + 256 * g : key1);
       }
     };
     int hb = 0;            // histogram buffer of unit u (u % NH, kept incrementally)
