@@ -165,6 +165,15 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, int32_t v) {
   asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// Predicated form: the predicate lives inside the asm, so the reduction stays one predicated
+// instruction (a C++ `if` around an asm statement becomes a divergent branch per reduction).
+__device__ __forceinline__ void red_add_shared_if(uint32_t addr, int32_t v, bool p) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.shared.add.s32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
+      "r"((int)p)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -240,6 +240,15 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     uint32_t gmask = 0;  // groups present in the key arrays (all but in the last warp)
 #pragma unroll
     for (int g = 0; g < NG; ++g) gmask |= (wr0 + 256 * g + 8 * lane < p.row_stride) ? (1u << g) : 0u;
+    // warp-uniform group classes of the warp holding the end of the rows: all 256 rows valid,
+    // some valid (the one group holding row `rows`), none
+    uint32_t full_groups = 0, part_groups = 0;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const int64_t g0 = wr0 + 256 * g;
+      if (g0 + 256 <= p.rows) full_groups |= 1u << g;
+      else if (g0 < p.rows) part_groups |= 1u << g;
+    }
     uint4 q0[NG], q1[NG];  // the current unit's keys; refilled group by group with the next unit's
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
@@ -287,19 +296,20 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       for (int e = 0; e < 4; ++e) {
         const int32_t x0 = vp[2 * e], x1 = vp[2 * e + 1];
         const uint32_t c0 = w4[e] & 0xffffu, c1 = w4[e] >> 16;
+        // SKIP0: predicated inside the asm (an `if` around it would branch per reduction)
+        auto red = [&](uint32_t a, int32_t val, int32_t x) {
+          if constexpr (SKIP0) red_add_shared_if(a, val, x != 0);
+          else red_add_shared(a, val);
+        };
         if constexpr (FX) {
           const uint32_t lo_off = (uint32_t)nbk * 4u;
-          if (!SKIP0 || x0 != 0) {
-            red_add_shared(Hs + c0, neg ? -(x0 >> 16) : (x0 >> 16));
-            red_add_shared(Hs + lo_off + c0, neg ? -(x0 & 0xffff) : (x0 & 0xffff));
-          }
-          if (!SKIP0 || x1 != 0) {
-            red_add_shared(Hs + c1, neg ? -(x1 >> 16) : (x1 >> 16));
-            red_add_shared(Hs + lo_off + c1, neg ? -(x1 & 0xffff) : (x1 & 0xffff));
-          }
+          red(Hs + c0, neg ? -(x0 >> 16) : (x0 >> 16), x0);
+          red(Hs + lo_off + c0, neg ? -(x0 & 0xffff) : (x0 & 0xffff), x0);
+          red(Hs + c1, neg ? -(x1 >> 16) : (x1 >> 16), x1);
+          red(Hs + lo_off + c1, neg ? -(x1 & 0xffff) : (x1 & 0xffff), x1);
         } else {
-          if (!SKIP0 || x0 != 0) red_add_shared(Hs + c0, neg ? -x0 : x0);
-          if (!SKIP0 || x1 != 0) red_add_shared(Hs + c1, neg ? -x1 : x1);
+          red(Hs + c0, neg ? -x0 : x0, x0);
+          red(Hs + c1, neg ? -x1 : x1, x1);
         }
       }
     };
@@ -314,8 +324,13 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 #pragma unroll
         for (int e = 0; e < 8; ++e) vp[e] = vr[g * 8 + e];
         if constexpr (SCHED) butterfly8(vp, sched_ctrl(q0[g].x, q0[g].y));
-        reduce_group(Hs, q0[g], vp, false, skip0);
-        if constexpr (TERNARY) reduce_group(Hs, q1[g], vp, true, skip0);
+        if (!decltype(skip0)::value || ((full_groups >> g) & 1u)) {  // every lane's 8 rows exist
+          reduce_group(Hs, q0[g], vp, false, std::false_type{});
+          if constexpr (TERNARY) reduce_group(Hs, q1[g], vp, true, std::false_type{});
+        } else if ((part_groups >> g) & 1u) {  // the group holding the last row: predicated
+          reduce_group(Hs, q0[g], vp, false, std::true_type{});
+          if constexpr (TERNARY) reduce_group(Hs, q1[g], vp, true, std::true_type{});
+        }  // else: every row of the group is past the end (warp-uniform skip)
         // branch-free (a shared guard lets the compiler merge the four loads and sink them to
         // the end of the unit, which leaves them no time): without a next unit, or for a group
         // past the key rows (its rows carry v = 0 and are skipped), load the array base instead
