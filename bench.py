@@ -262,6 +262,9 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     preprocess_s = time.perf_counter() - t0
 
+    # ---- the standard dense multiply on the GPU (2-bit planes, csrc/dense.cu): comparator
+    dense = rsr.DenseTernary(dA) if domain == "ternary" else None
+
     # ---- parity gate at full size (untimed): GPU keys + product vs the C oracle
     from oracle import c_oracle
     kp = c_oracle.keys_ternary(A, k, 1)
@@ -392,6 +395,31 @@ def run_ours(args, cfg):
     if not same(res):
         raise SystemExit("parity failure on the e2e path")
 
+    gpu_standard = None
+    if dense is not None:
+        dout = torch.empty(m, dtype=odt, device="cuda")
+        dense.multiply(dv, dout)
+        if not same(dout.cpu().numpy()):
+            raise SystemExit("parity failure: dense GPU product differs from the oracle")
+        dg = torch.cuda.CUDAGraph()
+        cap2 = torch.cuda.Stream()
+        cap2.wait_stream(stream)
+        with torch.cuda.stream(cap2), torch.cuda.graph(dg, stream=cap2):
+            for _ in range(min(args.steps, 200)):
+                dense.multiply(dv, dout)
+        stream.wait_stream(cap2)
+        dg.replay()
+        torch.cuda.synchronize()
+        t_begin.record(stream)
+        dg.replay()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        d_us = t_begin.elapsed_time(t_end) / min(args.steps, 200) * 1e3
+        gpu_standard = {"value": 1e6 / d_us, "unit": "vectors/s", "kernel_us": d_us,
+                        "weight_bytes": dense.nbytes,
+                        "what": "dense 2-bit ternary GEMV on the same GPU (the paper's standard multiply, csrc/dense.cu)"}
+        del dense
+
     peak, peak_kind = _peaks()
     avg_kernel_s = statistics.mean(kernel_ms) / 1e3
     # roofline.achieved counts the CANONICAL algorithmic bytes (u16 perm +
@@ -418,6 +446,8 @@ def run_ours(args, cfg):
                      "kernel_us": avg_kernel_s * 1e6},
         "clocks": clocks.summary(),
     }
+    if gpu_standard is not None:
+        line["gpu_standard"] = gpu_standard
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu_s, reps, workers, _ = time_cpu_reference(make_matrix(domain, n, m), v, k, domain,
                                                      min_seconds=args.cpu_seconds)

@@ -126,6 +126,18 @@ rsr_status rsr_index_import(const rsr_index_desc* desc, const uint32_t* d_perm0,
                             const uint32_t* d_perm1, const uint32_t* d_seg1, int64_t seg_stride,
                             void* workspace, size_t workspace_bytes, int32_t* d_error, void* stream);
 
+/* Dense 2-bit ternary GEMV — the paper's "standard" multiply (naive_multiply, core.py:135-169)
+ * on the GPU, kept as the honest comparator of the RSR path.
+ * rsr_dense_pack_ternary: int8 A [rows][lda] (device) -> bit-planes d_pos / d_neg, each
+ * rsr_dense_plane_words(rows, cols) u32 laid out [ceil(rows/32)][cols] (bit i of word
+ * [w][j] = A[32w+i][j] is +1 / -1); entries outside {-1,0,1} are counted into d_bad_entries.
+ * rsr_dense_multiply: out[cols] = v[rows] . A for int32 (exact) or fp32 v. */
+size_t rsr_dense_plane_words(int64_t rows, int64_t cols);
+rsr_status rsr_dense_pack_ternary(const int8_t* A, int64_t lda, int64_t rows, int64_t cols,
+                                  uint32_t* d_pos, uint32_t* d_neg, int32_t* d_bad_entries, void* stream);
+rsr_status rsr_dense_multiply(const uint32_t* d_pos, const uint32_t* d_neg, int64_t rows, int64_t cols,
+                              const void* v, rsr_dtype dtype, void* out, void* stream);
+
 /* Batched multiply: V [batch][rows] -> OUT [batch][cols] on the current stream, every index
  * byte read once per slice of up to 128 vectors instead of once per vector (SURVEY.md §8(d)
  * config 3; the reference has no batch API and runs `multiply_ternary`, kernels.py:196-206,

@@ -27,6 +27,7 @@ EXPORTS = (
     "rsr_index_import_workspace_bytes", "rsr_index_import",
     "rsr_multiply", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host", "rsr_segmented_sum",
     "rsr_block_product", "rsr_naive_multiply_ternary",
+    "rsr_dense_plane_words", "rsr_dense_pack_ternary", "rsr_dense_multiply",
 )
 
 
@@ -92,6 +93,12 @@ def lib() -> ctypes.CDLL:
     L.rsr_segmented_sum.restype = st
     L.rsr_block_product.argtypes = [P, I32_, ctypes.c_int, P, P, P]
     L.rsr_block_product.restype = st
+    L.rsr_dense_plane_words.argtypes = [I64, I64]
+    L.rsr_dense_plane_words.restype = SZ
+    L.rsr_dense_pack_ternary.argtypes = [P, I64, I64, I64, P, P, P, P]
+    L.rsr_dense_pack_ternary.restype = st
+    L.rsr_dense_multiply.argtypes = [P, P, I64, I64, P, ctypes.c_int, P, P]
+    L.rsr_dense_multiply.restype = st
     L.rsr_naive_multiply_ternary.argtypes = [P, I64, I64, I64, P, ctypes.c_int, P, P]
     L.rsr_naive_multiply_ternary.restype = st
     if L.rsr_b200_abi_version() != ABI_VERSION:

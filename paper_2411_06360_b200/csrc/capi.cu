@@ -25,6 +25,11 @@ rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t ld
 rsr_status block_product(const double* u, int w, int use_fold, double* buf, double* out, cudaStream_t s);
 size_t batched_workspace_bytes(const rsr_index_desc& d, int64_t batch, rsr_dtype dt);
 size_t index_import_workspace_bytes(const rsr_index_desc* d);
+size_t dense_plane_words(int64_t rows, int64_t cols);
+rsr_status dense_pack_ternary(const int8_t* A, int64_t lda, int64_t rows, int64_t cols, uint32_t* P, uint32_t* N,
+                              int32_t* bad, cudaStream_t s);
+rsr_status dense_multiply(const uint32_t* P, const uint32_t* N, int64_t rows, int64_t cols, const void* v,
+                          rsr_dtype dt, void* out, cudaStream_t s);
 rsr_status index_import(const rsr_index_desc* d, const uint32_t* perm0, const uint32_t* seg0, const uint32_t* perm1,
                         const uint32_t* seg1, int64_t seg_in_stride, void* ws, size_t ws_bytes, int32_t* err,
                         cudaStream_t s);
@@ -241,6 +246,18 @@ rsr_status rsr_segmented_sum(const rsr_index_desc* desc, int32_t half, int32_t b
   if (half < 0 || half >= desc->halves || block < 0 || block >= desc->nblocks)
     return fail(RSR_ERR_INVALID, "half or block out of range");
   return segmented_sum(*desc, half, block, v, dtype, u, (cudaStream_t)stream);
+}
+
+size_t rsr_dense_plane_words(int64_t rows, int64_t cols) { return rows > 0 && cols > 0 ? dense_plane_words(rows, cols) : 0; }
+
+rsr_status rsr_dense_pack_ternary(const int8_t* A, int64_t lda, int64_t rows, int64_t cols, uint32_t* d_pos,
+                                  uint32_t* d_neg, int32_t* d_bad_entries, void* stream) {
+  return dense_pack_ternary(A, lda, rows, cols, d_pos, d_neg, d_bad_entries, (cudaStream_t)stream);
+}
+
+rsr_status rsr_dense_multiply(const uint32_t* d_pos, const uint32_t* d_neg, int64_t rows, int64_t cols, const void* v,
+                              rsr_dtype dtype, void* out, void* stream) {
+  return dense_multiply(d_pos, d_neg, rows, cols, v, dtype, out, (cudaStream_t)stream);
 }
 
 rsr_status rsr_naive_multiply_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t lda, const void* v,

@@ -388,3 +388,22 @@ def test_bitlinear_decode_chain_graph(rsr, cuda):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(yg, y)
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (33, 7), (1000, 333), (4096, 4096), (2500, 1030)])
+def test_dense_standard_gemv(rsr, cuda, rows, cols):
+    """The dense 2-bit GPU GEMV (the paper's standard multiply, csrc/dense.cu) equals the
+    reference's naive_multiply (C port, core.py:135-143): int32 bitwise, fp32 within the bar."""
+    import torch
+    rng = np.random.default_rng([rows, cols, 77])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    D = rsr.DenseTernary(A)
+    vi = rng.integers(-100, 101, rows).astype(np.int32)
+    ref = c_oracle.naive_ternary(vi.astype(np.float64), A)
+    got = D.multiply(torch.from_numpy(vi).cuda()).cpu().numpy()
+    assert np.array_equal(got.astype(np.float64), ref)
+    vf = rng.standard_normal(rows).astype(np.float32)
+    reff = vf.astype(np.float64) @ A.astype(np.float64)
+    assert _fp32_ok(D.multiply(torch.from_numpy(vf).cuda()).cpu().numpy(), reff)
+    with pytest.raises(ValueError):
+        rsr.DenseTernary(np.full((4, 4), 2, np.int8))
