@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _native
 from .core import as_vector
-from .indexer import BlockIndex, RsrIndex, TernaryIndex
+from .indexer import BlockIndex, RsrIndex, TernaryIndex, column_blocks
 
 _VARIANTS = {"rsr": False, "rsrpp": True, "rsr++": True}
 
@@ -101,6 +101,43 @@ def block_product_rsr(u: SegmentedSums) -> np.ndarray:
 def block_product_rsrpp(u: SegmentedSums) -> np.ndarray:
     """Same value via the odd-sum / pairwise-compaction fold (kernels.py:111-116)."""
     return _block_product(u, True)
+
+
+# ---------------------------------------------------------------------------
+# instrumented twins (kernels.py:240-320): the same per-block device ops, plus the number of
+# accumulate steps the reference's loops perform — an audit of the work bound
+# n + 2*2^w - 2 per block (RSR++) / n + w*2^w (RSR)
+# ---------------------------------------------------------------------------
+
+def segmented_sum_counted(v, block: BlockIndex):
+    """(segmented_sum, adds): one accumulate per sorted position (kernels.py:244-262)."""
+    sums = segmented_sum(v, block)
+    return sums, int(block.permutation.shape[0])
+
+
+def block_product_rsr_counted(u: SegmentedSums):
+    """(block_product_rsr, width * 2^width) (kernels.py:265-277)."""
+    return block_product_rsr(u), u.width * (1 << u.width)
+
+
+def block_product_rsrpp_counted(u: SegmentedSums):
+    """(block_product_rsrpp, 2 * 2^width - 2) (kernels.py:280-302)."""
+    return block_product_rsrpp(u), 2 * (1 << u.width) - 2
+
+
+def multiply_counted(v, idx: RsrIndex, variant: str = "rsrpp"):
+    """Multiply via the per-block ops, returning (product, total accumulate count)
+    (kernels.py:305-320); bitwise equal to the reference's counted twin."""
+    use_fold = _use_fold(variant)
+    out = np.empty(idx.cols, np.float64)
+    total = 0
+    for (start, _), blk in zip(column_blocks(idx.cols, idx.k), idx.blocks):
+        sums, adds = segmented_sum_counted(v, blk)
+        total += adds
+        product, adds = block_product_rsrpp_counted(sums) if use_fold else block_product_rsr_counted(sums)
+        total += adds
+        out[start:start + blk.width] = product
+    return out, total
 
 
 # ---------------------------------------------------------------------------

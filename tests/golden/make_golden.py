@@ -191,6 +191,32 @@ def rsx_files() -> dict:
     return out
 
 
+def counted() -> dict:
+    """The reference's instrumented twins (kernels.py:240-320): products and accumulate counts."""
+    from rsr import kernels as K
+    out = {}
+    rng = np.random.default_rng(31)
+    for i, (rows, cols, k) in enumerate(((50, 23, 3), (300, 70, 6), (128, 9, 7))):
+        B = rng.integers(0, 2, size=(rows, cols)).astype(np.uint8)
+        idx = rsr.preprocess(rsr.BinaryMatrix.from_dense(B), k)
+        v = rng.standard_normal(rows)
+        out[f"c{i}_B"] = B
+        out[f"c{i}_k"] = np.int64(k)
+        out[f"c{i}_v"] = v
+        for variant in ("rsr", "rsrpp"):
+            y, total = K.multiply_counted(v, idx, variant)
+            out[f"c{i}_{variant}_y"] = y
+            out[f"c{i}_{variant}_total"] = np.int64(total)
+        sums, adds = K.segmented_sum_counted(v, idx.blocks[0])
+        out[f"c{i}_seg0_sums"] = sums.sums
+        out[f"c{i}_seg0_adds"] = np.int64(adds)
+        for name, fn in (("rsr", K.block_product_rsr_counted), ("rsrpp", K.block_product_rsrpp_counted)):
+            prod, adds = fn(sums)
+            out[f"c{i}_bp0_{name}"] = prod
+            out[f"c{i}_bp0_{name}_adds"] = np.int64(adds)
+    return out
+
+
 def main() -> None:
     np.savez_compressed(os.path.join(HERE, "worked_example.npz"), **worked_example())
     np.savez_compressed(os.path.join(HERE, "fuzz_small.npz"), **fuzz_cases(101, 60, 64, 8))
@@ -198,6 +224,7 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "folds.npz"), **folds())
     np.savez_compressed(os.path.join(HERE, "tuner.npz"), **tuner())
     np.savez_compressed(os.path.join(HERE, "rsx_products.npz"), **rsx_files())
+    np.savez_compressed(os.path.join(HERE, "counted.npz"), **counted())
     print("reference rsr", rsr.__version__, "golden vectors written to", HERE)
 
 

@@ -407,3 +407,23 @@ def test_dense_standard_gemv(rsr, cuda, rows, cols):
     assert _fp32_ok(D.multiply(torch.from_numpy(vf).cuda()).cpu().numpy(), reff)
     with pytest.raises(ValueError):
         rsr.DenseTernary(np.full((4, 4), 2, np.int8))
+
+
+def test_counted_twins_vs_reference(rsr, cuda):
+    """Instrumented twins (reference kernels.py:240-320): products bitwise equal to the
+    reference's counted twin and the same accumulate counts (n + 2*2^w - 2 per block for
+    RSR++, n + w*2^w for RSR)."""
+    import os
+    d = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "counted.npz"))
+    for i in range(3):
+        B, k, v = d[f"c{i}_B"], int(d[f"c{i}_k"]), d[f"c{i}_v"]
+        idx = rsr.preprocess(rsr.BinaryMatrix.from_dense(B), k)
+        for variant in ("rsr", "rsrpp"):
+            y, total = rsr.multiply_counted(v, idx, variant)
+            assert y.tobytes() == d[f"c{i}_{variant}_y"].tobytes(), (i, variant)
+            assert total == int(d[f"c{i}_{variant}_total"])
+        sums, adds = rsr.segmented_sum_counted(v, idx.blocks[0])
+        assert sums.sums.tobytes() == d[f"c{i}_seg0_sums"].tobytes() and adds == int(d[f"c{i}_seg0_adds"])
+        for name, fn in (("rsr", rsr.block_product_rsr_counted), ("rsrpp", rsr.block_product_rsrpp_counted)):
+            prod, adds = fn(sums)
+            assert prod.tobytes() == d[f"c{i}_bp0_{name}"].tobytes() and adds == int(d[f"c{i}_bp0_{name}_adds"])
