@@ -167,8 +167,12 @@ __device__ __forceinline__ int fx_exponent(const uint32_t* fxmax, int n) {
 // 16-bit limbs in two int32 histograms (integer atomics are native; fp32 shared atomics are a
 // CAS loop on sm_100).  Deterministic, and more accurate than fp32 summation.  Single row
 // split only (one scale per output column).
-template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, bool SCHED>
+// FW fold warps: 4 for full CTAs; 1 for small CTAs (<= 4 scatter warps, k <= 13) so that 4 of
+// them fit on an SM (the register budget stays that of the largest CTA: 96 per thread)
+template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, bool SCHED, int FW>
 __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
+  static_assert(FW == 1 || FW == 2 || FW == 4, "fold warps");
+  constexpr int FB = FW == 4 ? 2 : FW == 2 ? 1 : 0;  // key bits spanned by the fold warps
   static_assert(R % 8 == 0 && R * kScatterThreads <= 16384, "rows per CTA");
   constexpr int LIMBS = FX ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + ((sizeof(int32_t) * hist_words + 127) & ~(size_t)127));
   uint64_t* hfree = hfull + NH;
   uint32_t* fxmax = reinterpret_cast<uint32_t*>(hfree + NH);                   // [16] per-warp max |v| bits
-  long long* fxpart = reinterpret_cast<long long*>(fxmax + 16);                // [2][kFoldWarps][16]
+  long long* fxpart = reinterpret_cast<long long*>(fxmax + 16);                // [2][FW][16]
 
   const int split = blockIdx.x % p.n_splits;
   const int col_cta = blockIdx.x / p.n_splits;
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   if (t == 0) {
     for (int h = 0; h < NH; ++h) {
       mbar_init(&hfull[h], nwarps);
-      mbar_init(&hfree[h], kFoldWarps);
+      mbar_init(&hfree[h], FW);
     }
     fence_mbar_init();
   }
@@ -367,9 +371,9 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   } else {
     // ============================= fold warps =============================
     __syncthreads();
-    const int fw = warp - nwarps;  // fold warp index (kFoldWarps = 4: 2 warp bits)
+    const int fw = warp - nwarps;  // fold warp index (FB warp bits)
     // logical bin j = (fw*32 + lane) * 2^lb + e; lane bits start at lb, fold-warp bits at lb + 5
-    int lb = p.k - 5 - 2;
+    int lb = p.k - 5 - FB;  // <= 8
     if (lb < 0) lb = 0;
     const int fbase = (fw * 32 + lane) << lb;
     const bool active = fbase < nbk;
@@ -384,7 +388,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     int sh = -1;
     if (lane < 8) sh = lane < lb ? lane : -1;
     else if (lane < 13) sh = lb + (lane - 8);
-    else if (lane < 15) sh = lb + 5 + (lane - 13);
+    else if (lane < 13 + FB) sh = lb + 5 + (lane - 13);
     // per-lane partials of my bins of one limb histogram, then REDUX over the warp: lane i -> slot i
     auto fold_limb = [&](const int32_t* H) -> int32_t {
       int32_t a[8];  // local-bit partials, lb <= 7
@@ -457,8 +461,9 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         if (lane == 8 + bit) r = tv;
       }
       const int32_t W = __reduce_add_sync(0xffffffffu, X);
-      if (lane == 13) r = (fw & 1) ? W : 0;
-      if (lane == 14) r = (fw & 2) ? W : 0;
+#pragma unroll
+      for (int fb2 = 0; fb2 < FB; ++fb2)
+        if (lane == 13 + fb2) r = ((fw >> fb2) & 1) ? W : 0;
       return r;
     };
     int fb = 0;          // f % NH, kept incrementally
@@ -485,13 +490,13 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       const int w = block_width(p.cols, p.k, b);
       if constexpr (FX) {
         // exact fixed-point slot values from the 4 fold warps, summed in a fixed order
-        long long* fp = fxpart + (f & 1) * kFoldWarps * 16;
+        long long* fp = fxpart + (f & 1) * FW * 16;
         if (lane < 16) fp[fw * 16 + lane] = ((long long)d[0] << 16) + (long long)d[LIMBS - 1];
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * kFoldWarps) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
         if (fw == 0 && sh >= 0 && sh < w) {
           long long tot = 0;
 #pragma unroll
-          for (int i = 0; i < kFoldWarps; ++i) tot += fp[i * 16 + lane];
+          for (int i = 0; i < FW; ++i) tot += fp[i * 16 + lane];
           out[(int64_t)b * p.k + (w - 1 - sh)] = (OutT)ldexp((double)tot, -fx_e);
         }
       } else {
@@ -814,17 +819,17 @@ static bool pdl_enabled() {
   return on == 1;
 }
 
-template <bool PP, typename OutT, bool FX>
+template <bool PP, typename OutT, bool FX, int FW>
 rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
-  auto kern = p.halves == 2 ? (p.sched ? scatter_kernel<kScatterR, PP, true, OutT, FX, true>
-                                       : scatter_kernel<kScatterR, PP, true, OutT, FX, false>)
-                            : (p.sched ? scatter_kernel<kScatterR, PP, false, OutT, FX, true>
-                                       : scatter_kernel<kScatterR, PP, false, OutT, FX, false>);
+  auto kern = p.halves == 2 ? (p.sched ? scatter_kernel<kScatterR, PP, true, OutT, FX, true, FW>
+                                       : scatter_kernel<kScatterR, PP, true, OutT, FX, false, FW>)
+                            : (p.sched ? scatter_kernel<kScatterR, PP, false, OutT, FX, true, FW>
+                                       : scatter_kernel<kScatterR, PP, false, OutT, FX, false, FW>);
   rsr_status st = set_max_smem((const void*)kern, smem);
   if (st != RSR_OK) return st;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads + 32 * kFoldWarps);
+  cfg.blockDim = dim3(threads + 32 * FW);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -833,6 +838,12 @@ rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int t
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cuda_check(cudaLaunchKernelEx(&cfg, kern, p), "scatter_kernel launch");
+}
+
+template <bool PP, typename OutT, bool FX>
+rsr_status launch_scatter_fw(const ScatterParams& p, int grid, size_t smem, int threads, int fw, cudaStream_t s) {
+  return fw == 1 ? launch_scatter_t<PP, OutT, FX, 1>(p, grid, smem, threads, s)
+                 : launch_scatter_t<PP, OutT, FX, kFoldWarps>(p, grid, smem, threads, s);
 }
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, void* out, rsr_dtype out_dtype, bool pp,
@@ -877,7 +888,10 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   const size_t smem = need(nhist);
   // small CTAs (few rows) share an SM: limits from threads, smem and registers (<= 96 per
   // thread under the launch bounds)
-  const int cta_threads = threads + 32 * kFoldWarps;
+  // small CTAs run one fold warp so that 4 of them share an SM — when that puts every block in
+  // flight at once (with several blocks per CTA the single fold warp is the slower choice)
+  const int fw = (threads <= 128 && d.k <= 13 && (b1 - b0) <= 4 * device_sm_count()) ? 1 : kFoldWarps;
+  const int cta_threads = threads + 32 * fw;
   const int per_sm = std::max<int>(1, (int)std::min<size_t>(std::min(2048 / cta_threads, 65536 / (cta_threads * 96)),
                                                             (228u << 10) / (smem + 1024)));
   const int nblk = b1 - b0;
@@ -892,13 +906,13 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
     if (st != RSR_OK) return st;
   }
   if (fx)
-    return pp ? launch_scatter_t<true, float, true>(p, grid, smem, threads, s)
-              : launch_scatter_t<false, float, true>(p, grid, smem, threads, s);
+    return pp ? launch_scatter_fw<true, float, true>(p, grid, smem, threads, fw, s)
+              : launch_scatter_fw<false, float, true>(p, grid, smem, threads, fw, s);
   if (out_dtype == RSR_F64)
-    return pp ? launch_scatter_t<true, double, false>(p, grid, smem, threads, s)
-              : launch_scatter_t<false, double, false>(p, grid, smem, threads, s);
-  return pp ? launch_scatter_t<true, int32_t, false>(p, grid, smem, threads, s)
-            : launch_scatter_t<false, int32_t, false>(p, grid, smem, threads, s);
+    return pp ? launch_scatter_fw<true, double, false>(p, grid, smem, threads, fw, s)
+              : launch_scatter_fw<false, double, false>(p, grid, smem, threads, fw, s);
+  return pp ? launch_scatter_fw<true, int32_t, false>(p, grid, smem, threads, fw, s)
+            : launch_scatter_fw<false, int32_t, false>(p, grid, smem, threads, fw, s);
 }
 
 template <typename T>
