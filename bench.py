@@ -254,6 +254,8 @@ def run_ours(args, cfg):
     fp32 = args.config in FP32
     v = (np.random.default_rng([0, n, 2]).standard_normal(n).astype(np.float32) if fp32 else make_vector(n))
     dA = torch.from_numpy(A).cuda()
+    if domain == "ternary":  # first-use module loading of the preprocess kernels, untimed
+        rsr.preprocess_ternary(dA[:256, :64].contiguous(), k if k <= 8 else 8)
     torch.cuda.synchronize()
     t0 = time.perf_counter()  # preprocess only (the matrix is already in HBM)
     if domain == "ternary":
