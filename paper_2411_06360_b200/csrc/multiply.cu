@@ -1,32 +1,25 @@
 // sm_100a multiply kernels for RSR / RSR++ (arxiv 2411.06360).
 //
-// Two formulations of the reference hot loop, both computing, per column block
-// b of width w, the bucket sums u_b[j] and the block product r_b = u_b . Bin_w:
+// Two formulations of the reference hot loop, both computing, per column block b of width w,
+// the bucket sums u_b[j] and the block product r_b = u_b . Bin_w:
 //
-//  * SCATTER (int32 activations) — the reference's own fused driver
-//    `_run_blocks` (kernels.py:127-177): u_b[key_b[r]] += v[r] over rows r.
-//    One persistent CTA per SM keeps its slice of v in REGISTERS for the whole
-//    launch, streams the per-block key rows (u16, `_buckets`) into a shared-
-//    memory ring with 1-D TMA bulk copies (mbarrier completion, L2 evict_first),
-//    and accumulates a 2^k-bin histogram with shared-memory int32 atomics
-//    (native ATOMS.ADD on sm_100; measured as fast as a random LDS).  Ternary
-//    matrices scatter +v into the positive key's bin and -v into the negative
-//    key's bin of ONE histogram: the fold is linear, so fold(u+ - u-) equals
-//    the reference's `pos - neg` (kernels.py:206) exactly in integer arithmetic.
-//    One warp folds the finished histogram (RSR++ pairwise compaction,
-//    kernels.py:74-91, or the dense RSR product, kernels.py:63-71) while the
-//    other warps already scatter the next block into the second buffer.
+//  * SCATTER (int32, and fp32 as exact fixed point) — the reference's own fused driver
+//    `_run_blocks` (kernels.py:127-177): u_b[key_b[r]] += v[r] over rows r.  One persistent
+//    CTA per SM keeps its slice of v in REGISTERS for the whole launch, streams the per-block
+//    key codes straight into registers (L2 bulk prefetch a few blocks ahead), and accumulates
+//    a 2^k-bin histogram with shared-memory int32 reductions in a bank-conflict-minimising
+//    key order chosen at preprocess time (butterfly schedule).  Ternary matrices add +v at
+//    the positive key's bin and -v at the negative key's bin of ONE histogram: the fold is
+//    linear, so fold(u+ - u-) equals the reference's `pos - neg` (kernels.py:206) exactly.
+//    Dedicated fold warps reduce finished histograms (RSR++ pairwise compaction,
+//    kernels.py:74-91, or the dense RSR product, kernels.py:63-71) while the scatter warps
+//    fill the next buffer.
 //
-//  * GATHER (fp32 / fp64 / deterministic int32) — the paper's Eq. 4 form
-//    (`_segment_sums`, kernels.py:50-60): u[j] = sum over sorted positions
-//    p in [seg[j], seg[j+1]) of v[perm[p]].  v is staged in shared memory; one
-//    warp streams a block's perm in 256-position windows (8 positions per lane,
-//    one 16-byte load), gathers v, and computes window-local prefix sums with a
-//    warp-shuffle scan.  Each bucket boundary then contributes its window-local
-//    prefix with the RSR++ telescoping coefficients (bit_s(j-1) - bit_s(j)),
-//    i.e. the pairwise compaction of Alg. 3 applied to prefix sums (about two
-//    adds per bucket), or — for variant "rsr" — the segment sum u_j is formed
-//    and added to every column whose bit is set (w adds per bucket).  No
+//  * GATHER (fp64, and fp32 / int32 beyond the scatter limits) — the paper's Eq. 4 form
+//    (`_segment_sums`, kernels.py:50-60): u[j] = sum over sorted positions p in
+//    [seg[j], seg[j+1]) of v[perm[p]], v staged in shared memory, bucket boundaries folded
+//    with the RSR++ telescoping coefficients (bit_s(j-1) - bit_s(j)) of window-local prefix
+//    sums, or (variant "rsr") the segment sum added to every column whose bit is set.  No
 //    floating-point atomics: results are deterministic run to run.
 #include <cstdio>
 #include <cstdlib>
@@ -107,22 +100,6 @@ struct ScatterParams {
   int sched;          // keys stored in scheduled order (k <= 11): butterfly control bits in the codes
   uint32_t code_mask; // mask of the group's first two code words (clears the control bits)
 };
-
-template <typename OutT>
-__device__ __forceinline__ void emit(OutT* out, int64_t col, int32_t val, bool atomic) {
-  if (atomic) atomicAdd(out + col, (OutT)val);
-  else out[col] = (OutT)val;
-}
-
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 
 // Logical-order view of one int4 of swizzled bins: element e of the result is logical bin
 // 4q + e, given c = swizzle constant of the 32-bin group (key_swizzle XORs the low 5 bits).
