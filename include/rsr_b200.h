@@ -60,7 +60,12 @@ typedef struct rsr_half_index {
                        code = swz(key) << 2 for k <= 14 (swz(key) for k = 15, 16) where
                        swz(key) = key ^ ((key >> 5) & 31) is a shared-memory bank swizzle
                        (an involution) and << 2 makes the code the byte offset of the
-                       key's histogram word; padding rows hold 0 */
+                       key's histogram word; padding rows hold 0.  For k <= 11 the codes
+                       of every aligned 8-row group of whole 256-row chunks are stored in
+                       the scatter kernel's slot order: slot s holds row p[s], p = a
+                       3-stage butterfly of 12 control bits kept in bits 13-15 of the
+                       group's codes 0..3 (csrc/common.cuh butterfly8 / sched_ctrl;
+                       indexer.unschedule_codes restores row order) */
 } rsr_half_index;
 
 typedef struct rsr_index_desc {
@@ -69,7 +74,7 @@ typedef struct rsr_index_desc {
   int32_t nblocks;    /* ceil(cols / k) */
   int32_t perm_bytes; /* 2 or 4 */
   int32_t halves;     /* 1 = binary index; 2 = ternary (half[0] positive, half[1] negative) */
-  int64_t row_stride; /* rows rounded up to a multiple of 8 (16-byte rows for TMA) */
+  int64_t row_stride; /* rows rounded up to a multiple of 8 (16-byte aligned 8-row groups) */
   int64_t seg_stride; /* 2^k + 1 */
   rsr_half_index half[2];
 } rsr_index_desc;
