@@ -57,10 +57,10 @@ typedef struct rsr_half_index {
                        j < 2^w, seg[2^w] = rows (indexer.py:274-276 incl. sentinel) */
   uint16_t* bucket; /* [nblocks][row_stride]: key of every row, MSB-first
                        (indexer.py:270 `_buckets`), as a device code:
-                       code = swz(key) << 2 for k <= 14 (swz(key) for k = 15, 16) where
-                       swz(key) = key ^ ((key >> 5) & 31) is a shared-memory bank swizzle
-                       (an involution) and << 2 makes the code the byte offset of the
-                       key's histogram word; padding rows hold 0.  For k <= 11 the codes
+                       code = swz(key) << 2 for k <= 11 and k = 14 (the byte offset of the
+                       key's histogram word), swz(key) for k = 12, 13, 15, 16 (its word
+                       index), where swz(key) = key ^ ((key >> 5) & 31) is a shared-memory
+                       bank swizzle (an involution); padding rows hold 0.  For k <= 13 the codes
                        of every aligned 8-row group of whole 256-row chunks are stored in
                        the scatter kernel's slot order: slot s holds row p[s], p = a
                        3-stage butterfly of 12 control bits kept in bits 13-15 of the

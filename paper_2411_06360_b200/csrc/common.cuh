@@ -108,11 +108,16 @@ __host__ __device__ __forceinline__ uint32_t key_swizzle(uint32_t j) { return j 
 // Device code of a bucket key stored in the index: the swizzled key, pre-multiplied by 4
 // (the byte offset of its histogram word) when k <= 14 so the scatter loop needs one ALU
 // op per key.  k = 15, 16 keep the plain swizzled key (u16 range).
+// Device code of a key: the byte offset of its histogram word (swz(key) << 2) for k <= 11 and
+// k = 14, the word index swz(key) for k = 12, 13, 15, 16.  Codes of k <= 13 stay below 2^13, so
+// bits 13-15 are free for the key schedule's control bits.
+__host__ __device__ __forceinline__ int code_shift(int k) { return (k <= 11 || k == 14) ? 2 : 0; }
+__host__ __device__ __forceinline__ bool sched_keys(int k) { return k <= 13; }
 __host__ __device__ __forceinline__ uint32_t encode_key(uint32_t key, int k) {
-  return k <= 14 ? key_swizzle(key) << 2 : key_swizzle(key);
+  return key_swizzle(key) << code_shift(k);
 }
 __host__ __device__ __forceinline__ uint32_t decode_key(uint32_t code, int k) {
-  return key_swizzle(k <= 14 ? (code >> 2) : code);
+  return key_swizzle(code >> code_shift(k));
 }
 
 // Programmatic dependent launch (PDL): wait until the preceding grid in the stream has

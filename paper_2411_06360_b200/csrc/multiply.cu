@@ -97,7 +97,8 @@ struct ScatterParams {
   int rows_per_cta, n_splits, stages, atomic_out, nhist;
   int v_aligned;
   int scatter_warps;
-  int sched;          // keys stored in scheduled order (k <= 11): butterfly control bits in the codes
+  int sched;          // keys stored in scheduled order (k <= 13): butterfly control bits in the codes
+  int codes;          // code format: 0 byte offsets in row order, 1 scheduled byte offsets, 2 scheduled word indices
   uint32_t code_mask; // mask of the group's first two code words (clears the control bits)
 };
 
@@ -146,7 +147,9 @@ __device__ __forceinline__ int fx_exponent(const uint32_t* fxmax, int n) {
 // split only (one scale per output column).
 // FW fold warps: 4 for full CTAs; 1 for small CTAs (<= 4 scatter warps, k <= 13) so that 4 of
 // them fit on an SM (the register budget stays that of the largest CTA: 96 per thread)
-template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, bool SCHED, int FW>
+// CODES: 0 = byte-offset codes in row order (k = 14), 1 = scheduled byte-offset codes (k <= 11),
+// 2 = scheduled word-index codes (k = 12, 13; see common.cuh encode_key)
+template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, int CODES, int FW>
 __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
   static_assert(FW == 1 || FW == 2 || FW == 4, "fold warps");
   constexpr int FB = FW == 4 ? 2 : FW == 2 ? 1 : 0;  // key bits spanned by the fold warps
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       for (int i = 0; i < R; ++i) vr[i] = __float2int_rn(ldexpf(__int_as_float(vr[i]), e));
     }
     if (warp == 0) TRACE(1);
+    constexpr bool SCHED = CODES != 0;
     constexpr uint32_t kMask = SCHED ? kSchedCodeMask : 0xffffffffu;
     // the reductions of one half of one group: slot s adds +-vp[s] into the bin of code s.
     // SKIP0 (the warp holding the end of the rows): rows past the end carry v = 0 and their
@@ -276,7 +280,9 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int32_t x0 = vp[2 * e], x1 = vp[2 * e + 1];
-        const uint32_t c0 = w4[e] & 0xffffu, c1 = w4[e] >> 16;
+        // byte offsets of the two bins (word-index codes are scaled here)
+        const uint32_t c0 = CODES == 2 ? (w4[e] & 0xffffu) << 2 : w4[e] & 0xffffu;
+        const uint32_t c1 = CODES == 2 ? (w4[e] >> 16) << 2 : w4[e] >> 16;
         // SKIP0: predicated inside the asm (an `if` around it would branch per reduction)
         auto red = [&](uint32_t a, int32_t val, int32_t x) {
           if constexpr (SKIP0) red_add_shared_if(a, val, x != 0);
@@ -798,10 +804,13 @@ static bool pdl_enabled() {
 
 template <bool PP, typename OutT, bool FX, int FW>
 rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
-  auto kern = p.halves == 2 ? (p.sched ? scatter_kernel<kScatterR, PP, true, OutT, FX, true, FW>
-                                       : scatter_kernel<kScatterR, PP, true, OutT, FX, false, FW>)
-                            : (p.sched ? scatter_kernel<kScatterR, PP, false, OutT, FX, true, FW>
-                                       : scatter_kernel<kScatterR, PP, false, OutT, FX, false, FW>);
+  auto pick = [&](auto ternary) {
+    constexpr bool T = decltype(ternary)::value;
+    return p.codes == 1 ? scatter_kernel<kScatterR, PP, T, OutT, FX, 1, FW>
+           : p.codes == 2 ? scatter_kernel<kScatterR, PP, T, OutT, FX, 2, FW>
+                          : scatter_kernel<kScatterR, PP, T, OutT, FX, 0, FW>;
+  };
+  auto kern = p.halves == 2 ? pick(std::true_type{}) : pick(std::false_type{});
   rsr_status st = set_max_smem((const void*)kern, smem);
   if (st != RSR_OK) return st;
   cudaLaunchConfig_t cfg = {};
@@ -844,7 +853,8 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   while (threads < kScatterThreads && (int64_t)threads * R < d.rows) threads *= 2;
   p.rows_per_cta = threads * R;
   p.scatter_warps = threads / 32;
-  p.sched = d.k <= 11;
+  p.sched = sched_keys(d.k);
+  p.codes = !p.sched ? 0 : code_shift(d.k) == 2 ? 1 : 2;
   p.code_mask = p.sched ? kSchedCodeMask : 0xffffffffu;
   p.n_splits = (int)((d.rows + p.rows_per_cta - 1) / p.rows_per_cta);
   p.atomic_out = p.n_splits > 1;

@@ -166,7 +166,7 @@ rsr_status launch_sort(const rsr_index_desc& d, void* workspace, size_t ws_bytes
 }
 
 // ---------------------------------------------------------------------------------------
-// Key-order scheduling for the scatter kernel's shared-memory reductions (k <= 11).
+// Key-order scheduling for the scatter kernel's shared-memory reductions (k <= 13).
 // The scatter kernel issues one reduction instruction per (8-row group, slot s) with lane l
 // handling one row of its group 256c + 8l + [0, 8) of 256-row chunk c; the cost of an
 // instruction is the number of bank wavefronts = the largest number of lanes that hit one
@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(kSchedWarps * 32) schedule_keys_kernel(rsr_ind
   const int64_t c = task % nchunks;
   int (*cnt)[8][32] = cnt_all[wib];
   const int H = d.halves;
+  const int cs = code_shift(d.k);  // code -> histogram word index: code >> cs
   uint16_t* code[2] = {nullptr, nullptr};
   uint32_t kc[2][8] = {};
 #pragma unroll
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kSchedWarps * 32) schedule_keys_kernel(rsr_ind
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      if (h < H) atomicAdd(&cnt[h][e][(kc[h][e] >> 2) & 31], 1);
+      if (h < H) atomicAdd(&cnt[h][e][(kc[h][e] >> cs) & 31], 1);
   __syncwarp();
   uint32_t ctrl = 0;  // this lane's switches
   for (int sweep = 0; sweep < sweeps; ++sweep) {
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kSchedWarps * 32) schedule_keys_kernel(rsr_ind
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) bk[h][e] = __shfl_sync(0xffffffffu, (kc[h][e] >> 2) & 31, l);
+        for (int e = 0; e < 8; ++e) bk[h][e] = __shfl_sync(0xffffffffu, (kc[h][e] >> cs) & 31, l);
       uint32_t cur = __shfl_sync(0xffffffffu, ctrl, l);
       auto slot_banks = [&](uint32_t cc, uint32_t (&sb)[2][8]) {
 #pragma unroll
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(kSchedWarps * 32) schedule_keys_kernel(rsr_ind
 }
 
 rsr_status launch_schedule(const rsr_index_desc& d, cudaStream_t s) {
-  if (d.k > 11) return RSR_OK;  // no spare code bits: keys stay in row order
+  if (!sched_keys(d.k)) return RSR_OK;  // no spare code bits: keys stay in row order
   if (const char* e = getenv("RSR_B200_NOSCHED"))
     if (e[0] == '1') return RSR_OK;  // diagnostics
   const int64_t tasks = (int64_t)d.nblocks * (d.row_stride / 256);

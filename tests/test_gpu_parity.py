@@ -158,7 +158,7 @@ def test_zero_and_dense_extremes(rsr, cuda):
 def test_row_splits_and_large_k(rsr, cuda):
     """rows > 16384 exercises the multi-CTA row split (atomic output); k up to 15."""
     import torch
-    for rows, cols, k in ((20000, 40, 11), (40000, 33, 15), (16385, 30, 13)):
+    for rows, cols, k in ((20000, 40, 11), (40000, 33, 15), (16385, 30, 13), (16384, 29, 14), (8192, 26, 12)):
         rng = np.random.default_rng([rows, cols])
         A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
         v = rng.integers(-100, 101, size=rows).astype(np.int32)
