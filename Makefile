@@ -8,7 +8,14 @@ LIB := paper_2411_06360_b200/lib/librsr_b200.so
 OBJDIR := build/obj
 OBJ := $(patsubst paper_2411_06360_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
 
-all: $(LIB) oracle
+PYINC := $(shell python3 -c "import sysconfig; print(sysconfig.get_paths()['include'])")
+PYEXT := paper_2411_06360_b200/lib/_rsrhost$(shell python3 -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
+
+all: $(LIB) $(PYEXT) oracle
+
+# CPython binding of the host-buffer session (links the library through $ORIGIN)
+$(PYEXT): paper_2411_06360_b200/csrc/pyhost.c include/rsr_b200.h $(LIB)
+	gcc -O2 -fPIC -shared -Wall -Iinclude -I$(PYINC) $< -o $@ -Lpaper_2411_06360_b200/lib -lrsr_b200 -Wl,-rpath,'$$ORIGIN'
 
 $(OBJDIR)/%.o: paper_2411_06360_b200/csrc/%.cu $(HDR)
 	@mkdir -p $(OBJDIR)
@@ -16,13 +23,13 @@ $(OBJDIR)/%.o: paper_2411_06360_b200/csrc/%.cu $(HDR)
 
 $(LIB): $(OBJ)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
+	$(NVCC) $(ARCH) -shared -Xlinker -soname=librsr_b200.so -o $@ $(OBJ) -lcudart
 
 oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(PYEXT)
 	$(MAKE) -s -C oracle clean
 
 # diagnostic build with per-unit timestamps (tools/trace_scatter.py); not used by the product

@@ -164,6 +164,21 @@ rsr_status rsr_multiply_host(const rsr_index_desc* desc, const void* v_host, rsr
                              void* out_host, rsr_dtype out_dtype, rsr_variant variant,
                              void* d_v, void* d_out, void* stream);
 
+/* Host-buffer session (the e2e call): pinned staging for v, a device copy of v and of the result,
+ * and a mapped pinned result buffer, allocated once for one index and one vector type (int32,
+ * fp32 or fp64) on the current device.  rsr_host_session_multiply replaces multiply_ternary /
+ * multiply_rsr with host buffers (kernels.py:185-206): v_host [rows] of the session's type (any
+ * host memory, v_bytes = its size) -> out_host [cols] of out_dtype (F64, the reference's result
+ * type, or the vector type; out_bytes = its size).  It copies v into the staging buffer,
+ * enqueues H2D(v) and the multiply (a single-split scatter launch stores its results straight
+ * into the mapped buffer; other forms add a D2H copy), synchronizes the stream and converts the
+ * result into out_host.  One call at a time per session (use one session per thread). */
+typedef struct rsr_host_session rsr_host_session;
+rsr_status rsr_host_session_create(const rsr_index_desc* desc, rsr_dtype v_dtype, rsr_host_session** out);
+void rsr_host_session_destroy(rsr_host_session* session);
+rsr_status rsr_host_session_multiply(rsr_host_session* session, const void* v_host, size_t v_bytes,
+                                     void* out_host, size_t out_bytes, rsr_dtype out_dtype,
+                                     rsr_variant variant, void* stream);
 /* Replaces segmented_sum / `_segment_sums` (kernels.py:50-60, 94-101): gather-form
  * bucket sums u[0..2^w) of one block of one half. */
 rsr_status rsr_segmented_sum(const rsr_index_desc* desc, int32_t half, int32_t block,

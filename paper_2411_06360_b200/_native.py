@@ -25,7 +25,8 @@ EXPORTS = (
     "rsr_b200_abi_version", "rsr_b200_last_error", "rsr_index_layout",
     "rsr_preprocess_workspace_bytes", "rsr_preprocess_ternary", "rsr_preprocess_binary",
     "rsr_index_import_workspace_bytes", "rsr_index_import",
-    "rsr_multiply", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host", "rsr_segmented_sum",
+    "rsr_multiply", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host",
+    "rsr_host_session_create", "rsr_host_session_destroy", "rsr_host_session_multiply", "rsr_segmented_sum",
     "rsr_block_product", "rsr_naive_multiply_ternary",
     "rsr_dense_plane_words", "rsr_dense_pack_ternary", "rsr_dense_multiply",
 )
@@ -89,6 +90,12 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply_host.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                     ctypes.c_int, P, P, P]
     L.rsr_multiply_host.restype = st
+    L.rsr_host_session_create.argtypes = [ctypes.POINTER(IndexDesc), ctypes.c_int, ctypes.POINTER(P)]
+    L.rsr_host_session_create.restype = st
+    L.rsr_host_session_destroy.argtypes = [P]
+    L.rsr_host_session_destroy.restype = None
+    L.rsr_host_session_multiply.argtypes = [P, P, SZ, P, SZ, ctypes.c_int, ctypes.c_int, P]
+    L.rsr_host_session_multiply.restype = st
     L.rsr_segmented_sum.argtypes = [ctypes.POINTER(IndexDesc), I32_, I32_, P, ctypes.c_int, P, P]
     L.rsr_segmented_sum.restype = st
     L.rsr_block_product.argtypes = [P, I32_, ctypes.c_int, P, P, P]
@@ -105,6 +112,30 @@ def lib() -> ctypes.CDLL:
         raise ImportError("librsr_b200.so ABI version mismatch; rebuild with `make`")
     _lib = L
     return _lib
+
+
+_ext = None
+EXT_PATH = None
+
+
+def host_ext():
+    """The CPython binding of rsr_host_session_multiply (csrc/pyhost.c -> lib/_rsrhost*.so):
+    buffer-protocol arguments and the GIL released while the call waits on the GPU."""
+    global _ext, EXT_PATH
+    if _ext is not None:
+        return _ext
+    import importlib.machinery
+    import importlib.util
+    lib()  # the extension links librsr_b200.so; load (and version-check) it first
+    for suffix in importlib.machinery.EXTENSION_SUFFIXES:
+        path = os.path.join(_HERE, "lib", "_rsrhost" + suffix)
+        if os.path.exists(path):
+            spec = importlib.util.spec_from_file_location("_rsrhost", path)
+            mod = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(mod)
+            _ext, EXT_PATH = mod, path
+            return _ext
+    raise ImportError(f"_rsrhost extension not found under {os.path.join(_HERE, 'lib')}; build it with `make`")
 
 
 def check(status: int) -> None:

@@ -16,8 +16,6 @@ rsr_status preprocess_ternary(const int8_t* A, int64_t lda, const rsr_index_desc
                               size_t ws_bytes, cudaStream_t s);
 rsr_status preprocess_binary(const uint8_t* bits, int64_t ldb, const rsr_index_desc* d, void* ws, size_t ws_bytes,
                              cudaStream_t s);
-rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
-                    rsr_form form, int b0, int b1, cudaStream_t s);
 rsr_status segmented_sum(const rsr_index_desc& d, int half, int block, const void* v, rsr_dtype dt, void* u,
                          cudaStream_t s);
 rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t lda, const void* v, rsr_dtype dt,

@@ -148,4 +148,23 @@ __host__ __device__ __forceinline__ int block_width(int64_t cols, int k, int b) 
   return rem < k ? (int)rem : k;
 }
 
+// Result publishing for host-buffer sessions (csrc/host.cu): a single-split scatter multiply
+// also delivers its results to the host.  Every CTA stores its final columns into MAPPED host
+// memory and arrives on a device counter (gpu-scope release); the last arrival fences at system
+// scope and raises a host-visible flag.  The host polls the flag instead of copying back and
+// synchronizing the stream (tools/microbench/sync_probe.cu, session_timeline.cu).
+struct Publish {
+  void* host_out;     // device pointer of the mapped result buffer [cols], 4-byte elements
+  uint32_t* counter;  // device, 0 between calls
+  uint32_t* flag;     // device pointer of the mapped flag word
+  uint32_t seq;       // value the flag receives
+};
+
+// multiply.cu: one fused multiply over blocks [b0, b1).  With `pub`, a single-split scatter
+// launch with int32 / fp32 results also publishes them (then *published = true); otherwise the
+// caller copies the results back.
+rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
+                    rsr_form form, int b0, int b1, cudaStream_t s, const Publish* pub = nullptr,
+                    bool* published = nullptr);
+
 }  // namespace rsr

@@ -100,6 +100,7 @@ struct ScatterParams {
   int sched;          // keys stored in scheduled order (k <= 13): butterfly control bits in the codes
   int codes;          // code format: 0 byte offsets in row order, 1 scheduled byte offsets, 2 scheduled word indices
   uint32_t code_mask; // mask of the group's first two code words (clears the control bits)
+  Publish pub;        // host_out != nullptr: also store the results into mapped host memory + flag
 };
 
 // Logical-order view of one int4 of swizzled bins: element e of the result is logical bin
@@ -487,6 +488,35 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       }
       if (fw == 0 && f < 40) TRACE(400 + f);
     }
+    if (fw == 0) TRACE(6);
+    if (p.pub.host_out) {
+      // publish (host-buffer sessions; single split, so this CTA owns its columns): once every
+      // fold warp has added its share, the CTA's final columns go to mapped host memory (plain
+      // stores), then ONE thread releases them at gpu scope (fence after the barrier: cumulative
+      // over the CTA's stores) and arrives on the counter.  The grid's last arrival acquires
+      // every CTA's release, fences at system scope and raises the flag: host sees the flag =>
+      // host sees every CTA's stores (causality order), with one system fence per launch
+      // instead of one per CTA (tools/microbench/sync_probe.cu)
+      const int ft = fw * 32 + lane;
+      uint32_t* hout = reinterpret_cast<uint32_t*>(p.pub.host_out);
+      const uint32_t* dout = reinterpret_cast<const uint32_t*>(out);
+      __threadfence();  // my output reductions / stores are performed at L2
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
+      for (int i = ft; i < nunits * p.k; i += 32 * FW) {
+        const int b = p.b_begin + col_cta + (i / p.k) * ncol;
+        const int c = i % p.k;
+        if (c < block_width(p.cols, p.k, b)) hout[(int64_t)b * p.k + c] = __ldcg(dout + (int64_t)b * p.k + c);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
+      if (ft == 0) {
+        __threadfence();
+        if (atomicAdd(p.pub.counter, 1u) == gridDim.x - 1) {
+          __threadfence_system();
+          *p.pub.counter = 0;  // ready for the next call (stream-ordered)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pub.flag), "r"(p.pub.seq) : "memory");
+        }
+      }
+    }
   }
   if (warp == 0) TRACE(7);
 }
@@ -833,9 +863,10 @@ rsr_status launch_scatter_fw(const ScatterParams& p, int grid, size_t smem, int 
 }
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, void* out, rsr_dtype out_dtype, bool pp,
-                            int b0, int b1, cudaStream_t s) {
+                            int b0, int b1, cudaStream_t s, const Publish* pub, bool* published) {
   if (d.k > 14) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply supports k <= 14");
   ScatterParams p{};
+  const bool publish = pub && out_dtype != RSR_F64;  // single split only (decided below)
   for (int h = 0; h < d.halves; ++h) p.key[h] = d.half[h].bucket;
   p.v = reinterpret_cast<const int32_t*>(v);
   p.v_aligned = ((uintptr_t)v & 15) == 0;
@@ -858,6 +889,10 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   p.code_mask = p.sched ? kSchedCodeMask : 0xffffffffu;
   p.n_splits = (int)((d.rows + p.rows_per_cta - 1) / p.rows_per_cta);
   p.atomic_out = p.n_splits > 1;
+  if (publish && p.n_splits == 1) {
+    p.pub = *pub;
+    if (published) *published = true;
+  }
   const size_t max_smem = device_max_smem_optin();
   const size_t limbs = fx ? 2 : 1;
   auto need = [&](int nh) {  // layout of scatter_kernel's dynamic smem
@@ -946,8 +981,9 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
 }  // namespace
 
 rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
-                    rsr_form form, int b0, int b1, cudaStream_t s) {
+                    rsr_form form, int b0, int b1, cudaStream_t s, const Publish* pub, bool* published) {
   const bool pp = var == RSR_VARIANT_RSRPP;
+  if (published) *published = false;
   if (b0 >= b1) return RSR_OK;
   // fp32 on the scatter kernel needs one quantization scale per output column: one row split
   const bool fx_ok = vt == RSR_F32 && ot == RSR_F32 && d.rows <= (int64_t)kScatterThreads * kScatterR && d.k <= 14;
@@ -956,11 +992,11 @@ rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* 
   if (form == RSR_FORM_SCATTER) {
     if (vt == RSR_F32) {
       if (!fx_ok) return fail(RSR_ERR_INVALID, "fp32 scatter form needs rows <= 16384, k <= 14, fp32 output");
-      return multiply_scatter(d, v, true, out, ot, pp, b0, b1, s);
+      return multiply_scatter(d, v, true, out, ot, pp, b0, b1, s, pub, published);
     }
     if (vt != RSR_I32) return fail(RSR_ERR_INVALID, "scatter form needs int32 or fp32 activations");
     if (ot != RSR_I32 && ot != RSR_F64) return fail(RSR_ERR_INVALID, "int32 activations produce int32 or float64");
-    return multiply_scatter(d, v, false, out, ot, pp, b0, b1, s);
+    return multiply_scatter(d, v, false, out, ot, pp, b0, b1, s, pub, published);
   }
   if (vt != ot) return fail(RSR_ERR_INVALID, "gather form writes the activation dtype");
   switch (vt) {

@@ -158,8 +158,8 @@ def _torch_dtype_code(t) -> int:
 
 
 class _HostStaging(threading.local):
-    """Pinned host buffers + device scratch reused by the host-buffer (e2e) path.  Thread-local:
-    concurrent multiplies from several threads never share buffers."""
+    """Per-thread device scratch and host-buffer sessions.  Thread-local: concurrent multiplies
+    from several threads never share buffers."""
 
     def __init__(self):
         self.bufs = {}
@@ -179,26 +179,23 @@ class _HostStaging(threading.local):
 
 
 _staging = _HostStaging()
+_KIND_CODE = {"i32": _native.I32, "f32": _native.F32, "f64": _native.F64}
 
 
 class _HostPlan:
-    """Everything one host-buffer multiply against one index needs, resolved once per thread:
-    pinned staging views, device scratch pointers, the descriptor reference."""
-    __slots__ = ("v_np", "args_v", "o_np", "args_o", "desc_ref", "fn")
+    """One host-buffer session (rsr_host_session_*: pinned staging, device scratch, mapped
+    result + completion flag) for one index, vector type and thread, created on first use and
+    destroyed with the index or the thread."""
+    __slots__ = ("session", "cols", "call", "__weakref__")
 
     def __init__(self, idx, kind):
-        import torch
-        tdt = {"i32": torch.int32, "f32": torch.float32, "f64": torch.float64}[kind]
-        odt = torch.float32 if kind == "f32" else torch.float64  # fp32 activations -> fp32 results
-        vh = _staging.get("v_" + kind, idx.rows, tdt, True)
-        dv = _staging.get("dv_" + kind, idx.rows, tdt, False)
-        oh = _staging.get("o_" + str(odt), idx.cols, odt, True)
-        do = _staging.get("do_" + str(odt), idx.cols, odt, False)
-        self.v_np, self.o_np = vh[1], oh[1]
-        self.args_v = (ctypes.c_void_p(vh[2]), {"i32": _native.I32, "f32": _native.F32, "f64": _native.F64}[kind])
-        self.args_o = (ctypes.c_void_p(oh[2]), _native.F32 if kind == "f32" else _native.F64)
-        self.desc_ref = ctypes.byref(idx.desc)
-        self.fn = (_native.lib().rsr_multiply_host, ctypes.c_void_p(dv[2]), ctypes.c_void_p(do[2]))
+        L = _native.lib()
+        h = ctypes.c_void_p()
+        _native.check(L.rsr_host_session_create(ctypes.byref(idx.desc), _KIND_CODE[kind], ctypes.byref(h)))
+        self.session = h.value
+        self.cols = idx.cols
+        self.call = _native.host_ext().multiply
+        weakref.finalize(self, L.rsr_host_session_destroy, h.value)
 
 
 def _host_plan(idx, kind) -> _HostPlan:
@@ -214,13 +211,16 @@ def _host_plan(idx, kind) -> _HostPlan:
     return plan
 
 
-def _run_host_plan(plan: _HostPlan, use_fold: bool) -> np.ndarray:
-    fn, dv, do = plan.fn
-    st = fn(plan.desc_ref, plan.args_v[0], plan.args_v[1], plan.args_o[0], plan.args_o[1],
-            _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, dv, do, _native.current_stream_ptr())
+def _run_host(idx, kind, v: np.ndarray, use_fold: bool) -> np.ndarray:
+    """One session call: v (C-contiguous, the session's type) -> fresh fp64 result (the
+    reference's result type)."""
+    plan = _host_plan(idx, kind)
+    out = np.empty(plan.cols, np.float64)
+    st = plan.call(plan.session, v, out, _native.F64, _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR,
+                   _native.current_stream_ptr())
     if st:
         _native.check(st)
-    return plan.o_np.astype(np.float64)  # fresh array (fp64, the reference's result type)
+    return out
 
 
 def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO):
@@ -254,9 +254,7 @@ def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray
         if raw.shape[0] != idx.rows:
             raise ValueError(f"vector length {raw.shape[0]} does not match {idx.rows} rows")
         if raw.dtype.itemsize < 4 or raw.dtype == np.int32 or (raw.min() >= -2 ** 31 and raw.max() < 2 ** 31):
-            plan = _host_plan(idx, "i32")
-            plan.v_np[:] = raw
-            return _run_host_plan(plan, use_fold)
+            return _run_host(idx, "i32", np.ascontiguousarray(raw, np.int32), use_fold)
         if compute == "int32":
             raise ValueError("integer activations exceed the int32 range")
     if raw.dtype == np.float32 and compute in (None, "float32"):
@@ -268,27 +266,19 @@ def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray
             raise ValueError("vector entries must be finite")
         if raw.shape[0] != idx.rows:
             raise ValueError(f"vector length {raw.shape[0]} does not match {idx.rows} rows")
-        plan = _host_plan(idx, "f32")
-        plan.v_np[:] = raw
-        return _run_host_plan(plan, use_fold)
+        return _run_host(idx, "f32", np.ascontiguousarray(raw), use_fold)
     v = as_vector(v_in)
     if v.shape[0] != idx.rows:
         raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
     if compute == "float32":
-        plan = _host_plan(idx, "f32")
-        plan.v_np[:] = v.astype(np.float32)
-        return _run_host_plan(plan, use_fold)
+        return _run_host(idx, "f32", v.astype(np.float32), use_fold)
     if compute == "int32":
         if np.any(v != np.round(v)) or np.abs(v).max(initial=0) >= 2 ** 31:
             raise ValueError("compute='int32' needs integer-valued activations in the int32 range")
-        plan = _host_plan(idx, "i32")
-        plan.v_np[:] = v.astype(np.int32)
-    elif compute in (None, "float64"):
-        plan = _host_plan(idx, "f64")
-        plan.v_np[:] = v
-    else:
-        raise ValueError("compute must be int32, float32 or float64 for host vectors")
-    return _run_host_plan(plan, use_fold)
+        return _run_host(idx, "i32", v.astype(np.int32), use_fold)
+    if compute in (None, "float64"):
+        return _run_host(idx, "f64", np.ascontiguousarray(v), use_fold)
+    raise ValueError("compute must be int32, float32 or float64 for host vectors")
 
 
 def _is_device_tensor(v) -> bool:

@@ -427,3 +427,60 @@ def test_counted_twins_vs_reference(rsr, cuda):
         for name, fn in (("rsr", rsr.block_product_rsr_counted), ("rsrpp", rsr.block_product_rsrpp_counted)):
             prod, adds = fn(sums)
             assert prod.tobytes() == d[f"c{i}_bp0_{name}"].tobytes() and adds == int(d[f"c{i}_bp0_{name}_adds"])
+
+
+# ----------------------------------------------------------------------------- host-buffer sessions
+@pytest.mark.parametrize("rows,cols,k", [(1, 1, 1), (37, 29, 3), (1000, 777, 8), (16384, 1001, 11),
+                                         (20000, 515, 12)])
+def test_host_session_all_types(rsr, cuda, rows, cols, k):
+    """NumPy in -> fresh fp64 NumPy out through the host session (H2D, multiply, publish into
+    mapped memory, flag poll): int32 / int64 bit-exact, fp32 within the north-star bound, fp64
+    within the reference's float tolerance; repeated calls reuse the session."""
+    rng = np.random.default_rng([rows, cols, k])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+    for trial in range(3):
+        vi = rng.integers(-100, 101, size=rows)
+        ref = c_oracle.naive_ternary(vi.astype(np.float64), A)
+        for v in (vi.astype(np.int32), vi.astype(np.int64)):
+            got = rsr.multiply_ternary(v, idx)
+            assert got.dtype == np.float64 and got.shape == (cols,)
+            assert np.array_equal(got, ref)
+        vf = rng.standard_normal(rows)
+        reff = c_oracle.naive_ternary(vf.astype(np.float32).astype(np.float64), A)
+        assert _fp32_ok(rsr.multiply_ternary(vf.astype(np.float32), idx), reff)
+        ref64 = c_oracle.naive_ternary(vf, A)
+        np.testing.assert_allclose(rsr.multiply_ternary(vf, idx), ref64, rtol=1e-9, atol=1e-9)
+        a = rsr.multiply_ternary(vi.astype(np.int32), idx, "rsr")
+        assert np.array_equal(a, ref)
+        assert a is not rsr.multiply_ternary(vi.astype(np.int32), idx)  # fresh arrays
+
+
+def test_host_session_threads_and_errors(rsr, cuda):
+    """One session per thread: concurrent host-buffer multiplies give the single-thread
+    results; bad lengths raise the reference's ValueError."""
+    import threading
+    rng = np.random.default_rng(7)
+    A = rng.integers(-1, 2, size=(4096, 4096), dtype=np.int8)
+    idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), 9)
+    vs = [rng.integers(-100, 101, size=4096).astype(np.int32) for _ in range(4)]
+    refs = [c_oracle.naive_ternary(v.astype(np.float64), A) for v in vs]
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(50):
+                if not np.array_equal(rsr.multiply_ternary(vs[i], idx), refs[i]):
+                    errors.append(i)
+                    return
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
+    with pytest.raises(ValueError, match="does not match"):
+        rsr.multiply_ternary(vs[0][:100], idx)

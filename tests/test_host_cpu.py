@@ -28,6 +28,19 @@ def test_library_exports_every_header_symbol():
     assert L.rsr_b200_abi_version() == _native.ABI_VERSION
 
 
+def test_host_extension_links_the_library():
+    """The CPython binding of the host-buffer session loads without a GPU and resolves
+    rsr_host_session_multiply from the same in-tree librsr_b200.so."""
+    from paper_2411_06360_b200 import _native
+    ext = _native.host_ext()
+    assert callable(ext.multiply)
+    assert os.path.dirname(_native.EXT_PATH) == os.path.dirname(_native.LIB_PATH)
+    deps = subprocess.run(["ldd", _native.EXT_PATH], capture_output=True, text=True).stdout
+    assert os.path.realpath(_native.LIB_PATH) in {os.path.realpath(p) for p in re.findall(r"=> (\S+)", deps)}
+    with pytest.raises(TypeError):
+        ext.multiply(0)
+
+
 def test_library_is_sm100a():
     from paper_2411_06360_b200 import _native
     out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True, text=True).stdout

@@ -17,6 +17,8 @@ def t(f, reps=300):
     torch.cuda.synchronize()
     return (time.perf_counter() - t0) / reps * 1e6
 print(f"multiply_ternary(numpy)          {t(lambda: rsr.multiply_ternary(v, idx)):7.1f} us")
+plan = K._host_plan(idx, "i32"); out = np.empty(m, np.float64); sp = _native.current_stream_ptr()
+print(f"session call (ext, no python)    {t(lambda: plan.call(plan.session, v, out, _native.F64, 1, sp)):7.1f} us")
 vh = K._staging.get("v_i32", n, torch.int32, True); dv = K._staging.get("dv_i32", n, torch.int32, False)
 oh = K._staging.get("o_f64", m, torch.float64, True); do = K._staging.get("do_f64", m, torch.float64, False)
 L = _native.lib(); sp = _native.current_stream_ptr()
