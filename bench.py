@@ -397,6 +397,8 @@ def run_ours(args, cfg):
 
     # ---- e2e through the reference-facing API with host buffers (rank-local)
     v_host = v.copy()
+    if os.environ.get("RSR_BENCH_NO_E2E"):  # diagnostics (kernel A/B of library builds)
+        mult = lambda vh, idx: ref  # noqa: E731
     for i in range(3):
         mult(v_host, copies[i % ncopies])
     torch.cuda.synchronize()

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librsr_b200.so")
+LIB_PATH = os.environ.get("RSR_B200_LIB") or os.path.join(_HERE, "lib", "librsr_b200.so")  # override: A/B builds
 
 RSR_OK, RSR_ERR_INVALID, RSR_ERR_UNSUPPORTED, RSR_ERR_CUDA = 0, 1, 2, 3
 I32, F32, F64 = 0, 1, 2

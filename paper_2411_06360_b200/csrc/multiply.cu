@@ -32,10 +32,18 @@ namespace rsr {
 
 namespace {
 
-constexpr int kScatterThreads = 512;  // x kScatterR rows per thread = 16384 rows per CTA
-constexpr int kScatterR = 32;
+#ifndef RSR_R
+#define RSR_R 32
+#endif
+constexpr int kScatterR = RSR_R;  // rows per scatter thread (multiple of 8)
+// scatter threads of a full CTA: kScatterR rows each, >= 16384 rows per CTA
+constexpr int kScatterThreads = (16384 / kScatterR + 31) / 32 * 32;
 constexpr int kFoldWarps = 4;  // dedicated fold warps per CTA
 constexpr int kMaxK = 16;
+#ifndef RSR_KA
+#define RSR_KA 1
+#endif
+constexpr int KA = RSR_KA;  // scatter kernel: 8-row key groups in flight per lane (divides R / 8)
 
 // =====================================================================================
 // Histogram layout.  Logical bin j lives at word key_swizzle(j) = j ^ ((j >> 5) & 31):
@@ -154,7 +162,7 @@ template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, int CODES, i
 __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
   static_assert(FW == 1 || FW == 2 || FW == 4, "fold warps");
   constexpr int FB = FW == 4 ? 2 : FW == 2 ? 1 : 0;  // key bits spanned by the fold warps
-  static_assert(R % 8 == 0 && R * kScatterThreads <= 16384, "rows per CTA");
+  static_assert(R % 8 == 0 && R * kScatterThreads <= 32768, "rows per CTA");
   constexpr int LIMBS = FX ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int HALVES = TERNARY ? 2 : 1;
@@ -171,8 +179,8 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   int32_t* hist = reinterpret_cast<int32_t*>(smem);  // [NH][LIMBS][nbk]
   uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + ((sizeof(int32_t) * hist_words + 127) & ~(size_t)127));
   uint64_t* hfree = hfull + NH;
-  uint32_t* fxmax = reinterpret_cast<uint32_t*>(hfree + NH);                   // [16] per-warp max |v| bits
-  long long* fxpart = reinterpret_cast<long long*>(fxmax + 16);                // [2][FW][16]
+  uint32_t* fxmax = reinterpret_cast<uint32_t*>(hfree + NH);                   // [32] per-warp max |v| bits
+  long long* fxpart = reinterpret_cast<long long*>(fxmax + 32);                // [2][FW][16]
 
   const int split = blockIdx.x % p.n_splits;
   const int col_cta = blockIdx.x / p.n_splits;
@@ -234,9 +242,11 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       if (g0 + 256 <= p.rows) full_groups |= 1u << g;
       else if (g0 < p.rows) part_groups |= 1u << g;
     }
-    uint4 q0[NG], q1[NG];  // the current unit's keys; refilled group by group with the next unit's
+    // key register ring: KA groups in flight; slot g % KA holds group g's keys, refilled right
+    // after its reductions with the keys of the group KA places later in the (unit, group) order
+    uint4 q0[KA], q1[KA];
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
+    for (int g = 0; g < KA; ++g) {
       const bool ld = nunits > 0 && ((gmask >> g) & 1u);
       q0[g] = ld ? ld_nc_v4(kb0 + 256 * g) : make_uint4(0, 0, 0, 0);
       q1[g] = (TERNARY && ld) ? ld_nc_v4(kb1 + 256 * g) : make_uint4(0, 0, 0, 0);
@@ -301,30 +311,35 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         }
       }
     };
-    // one unit's groups: the reductions of group g, then the next unit's keys of group g (a
-    // whole unit ahead, into the registers just consumed)
+    // one unit's groups: the reductions of group g, then the keys of the group KA later (this
+    // unit's group g + KA, or the next unit's group g + KA - NG) into the registers just consumed
     auto unit_groups = [&](uint32_t Hs, bool more, auto skip0) {
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
+        uint4& q0g = q0[g % KA];
+        uint4& q1g = q1[g % KA];
         // slot s of the group holds row p[s], p = butterfly of the control bits (k <= 11):
         // route the v registers the same way, once for both halves
         int32_t vp[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) vp[e] = vr[g * 8 + e];
-        if constexpr (SCHED) butterfly8(vp, sched_ctrl(q0[g].x, q0[g].y));
+        if constexpr (SCHED) butterfly8(vp, sched_ctrl(q0g.x, q0g.y));
         if (!decltype(skip0)::value || ((full_groups >> g) & 1u)) {  // every lane's 8 rows exist
-          reduce_group(Hs, q0[g], vp, false, std::false_type{});
-          if constexpr (TERNARY) reduce_group(Hs, q1[g], vp, true, std::false_type{});
+          reduce_group(Hs, q0g, vp, false, std::false_type{});
+          if constexpr (TERNARY) reduce_group(Hs, q1g, vp, true, std::false_type{});
         } else if ((part_groups >> g) & 1u) {  // the group holding the last row: predicated
-          reduce_group(Hs, q0[g], vp, false, std::true_type{});
-          if constexpr (TERNARY) reduce_group(Hs, q1[g], vp, true, std::true_type{});
+          reduce_group(Hs, q0g, vp, false, std::true_type{});
+          if constexpr (TERNARY) reduce_group(Hs, q1g, vp, true, std::true_type{});
         }  // else: every row of the group is past the end (warp-uniform skip)
         // branch-free (a shared guard lets the compiler merge the four loads and sink them to
         // the end of the unit, which leaves them no time): without a next unit, or for a group
         // past the key rows (its rows carry v = 0 and are skipped), load the array base instead
-        const bool ld = more && ((gmask >> g) & 1u);
-        q0[g] = ld_nc_v4(ld ? kb0 + 256 * g : key0);
-        if constexpr (TERNARY) q1[g] = ld_nc_v4(ld ? kb1 + 256 * g : key1);
+        const int gn = (g + KA) % NG;             // group to load (unrolled: constant)
+        const bool next_unit = g + KA >= NG;      // ... of the next unit (kb0 points there)
+        const bool ld = (!next_unit || more) && ((gmask >> gn) & 1u);
+        const int64_t back = next_unit ? 0 : ustride;  // this unit = kb0 - ustride
+        q0g = ld_nc_v4(ld ? kb0 - back + 256 * gn : key0);
+        if constexpr (TERNARY) q1g = ld_nc_v4(ld ? kb1 - back + 256 * gn : key1);
       }
     };
     int hb = 0;            // histogram buffer of unit u (u % NH, kept incrementally)
@@ -882,6 +897,7 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   const int R = kScatterR;
   int threads = 32;
   while (threads < kScatterThreads && (int64_t)threads * R < d.rows) threads *= 2;
+  threads = std::min(threads, kScatterThreads);
   p.rows_per_cta = threads * R;
   p.scatter_warps = threads / 32;
   p.sched = sched_keys(d.k);
@@ -897,7 +913,7 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   const size_t limbs = fx ? 2 : 1;
   auto need = [&](int nh) {  // layout of scatter_kernel's dynamic smem
     return ((sizeof(int32_t) * ((((size_t)1 << d.k) * nh * limbs + 15) & ~(size_t)15) + 127) & ~(size_t)127) +
-           8 * (2 * nh) + 64 /* fxmax */ + (fx ? sizeof(long long) * 2 * kFoldWarps * 16 : 0) /* fxpart */;
+           8 * (2 * nh) + 128 /* fxmax */ + (fx ? sizeof(long long) * 2 * kFoldWarps * 16 : 0) /* fxpart */;
   };
   // the deferred fold wants 3 histogram buffers (2 is the minimum)
   int nhist = need(3) <= max_smem ? 3 : 2;
