@@ -399,7 +399,7 @@ def run_ours(args, cfg):
     v_host = v.copy()
     if os.environ.get("RSR_BENCH_NO_E2E"):  # diagnostics (kernel A/B of library builds)
         mult = lambda vh, idx: ref  # noqa: E731
-    for i in range(3):
+    for i in range(max(3, ncopies)):  # untimed: every copy's host session (pinned buffers) exists
         mult(v_host, copies[i % ncopies])
     torch.cuda.synchronize()
     e2e_steps = min(max(args.steps, 20), 500)

@@ -205,7 +205,8 @@ rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_d
     // fixed-point limits)
     const bool scatter = desc->k <= 14 && (v_dtype == RSR_I32 || desc->rows <= 16384);
     loop = index_bytes <= ((size_t)96 << 20) && scatter && out_dtype == v_dtype;
-    if (const char* e = getenv("RSR_B200_BATCH_FORM")) loop = e[0] == 'l';
+    static const char* env_form = getenv("RSR_B200_BATCH_FORM");  // diagnostics, read once
+    if (env_form) loop = env_form[0] == 'l';
   }
   if (loop) {  // one multiply per vector
     const size_t vsz = v_dtype == RSR_F64 ? 8 : 4, osz = out_dtype == RSR_F64 ? 8 : 4;

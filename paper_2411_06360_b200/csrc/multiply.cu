@@ -145,8 +145,21 @@ __device__ __forceinline__ int fx_exponent(const uint32_t* fxmax, int n) {
   uint32_t m = 0;
   for (int i = 0; i < n; ++i) m = max(m, fxmax[i]);
   if (m == 0) return 0;
-  const float mf = __uint_as_float(m);
-  return 29 - ilogbf(mf);  // mf < 2^(ilogb+1) -> |v| * 2^e < 2^30
+  // ilogb of the max (finite, positive float bits), denormals included
+  const int lg = (m >> 23) ? (int)(m >> 23) - 127 : (31 - __clz((int)m)) - 149;
+  return 29 - lg;  // max < 2^(lg+1) -> |v| * 2^e < 2^30
+}
+
+// x * 2^e, exact (power-of-two scaling of a value whose result is normal): one or two
+// multiplies by power-of-two constants built from the exponent bits (ldexpf is a software
+// routine with special-case branches, measured ~3 us of the FX prologue at 4096 rows)
+__device__ __forceinline__ float scale_pow2(float x, int e) {
+  if (e >= -126 && e <= 127) return x * __int_as_float((127 + e) << 23);
+  const int h = e / 2;
+  return (x * __int_as_float((127 + h) << 23)) * __int_as_float((127 + (e - h)) << 23);
+}
+__device__ __forceinline__ double pow2d(int e) {  // 2^e for |e| <= 1022
+  return __longlong_as_double((long long)(1023 + e) << 52);
 }
 
 // FX (fp32 activations): v is quantized once per launch to 31-bit fixed point with a per-CTA
@@ -277,7 +290,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     if constexpr (FX) {
       const int e = fx_exponent(fxmax, nwarps);
 #pragma unroll
-      for (int i = 0; i < R; ++i) vr[i] = __float2int_rn(ldexpf(__int_as_float(vr[i]), e));
+      for (int i = 0; i < R; ++i) vr[i] = __float2int_rn(scale_pow2(__int_as_float(vr[i]), e));
     }
     if (warp == 0) TRACE(1);
     constexpr bool SCHED = CODES != 0;
@@ -496,7 +509,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
           long long tot = 0;
 #pragma unroll
           for (int i = 0; i < FW; ++i) tot += fp[i * 16 + lane];
-          out[(int64_t)b * p.k + (w - 1 - sh)] = (OutT)ldexp((double)tot, -fx_e);
+          out[(int64_t)b * p.k + (w - 1 - sh)] = (OutT)((double)tot * pow2d(-fx_e));
         }
       } else {
         if (sh >= 0 && sh < w && d[0] != 0) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)d[0]);
@@ -918,9 +931,11 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   // the deferred fold wants 3 histogram buffers (2 is the minimum)
   int nhist = need(3) <= max_smem ? 3 : 2;
   if (need(nhist) > max_smem) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply: histograms do not fit in shared memory");
-  int stages = 3;  // L2 prefetch distance in blocks
-  if (const char* e = getenv("RSR_B200_STAGES")) stages = std::max(0, atoi(e));  // diagnostics
-  if (const char* e = getenv("RSR_B200_NHIST")) nhist = std::min(4, std::max(2, atoi(e)));
+  // diagnostics overrides, read once (an environment scan per launch costs ~1 us of host time)
+  static const int env_stages = getenv("RSR_B200_STAGES") ? std::max(0, atoi(getenv("RSR_B200_STAGES"))) : -1;
+  static const int env_nhist = getenv("RSR_B200_NHIST") ? std::min(4, std::max(2, atoi(getenv("RSR_B200_NHIST")))) : -1;
+  const int stages = env_stages >= 0 ? env_stages : 3;  // L2 prefetch distance in blocks
+  if (env_nhist > 0) nhist = env_nhist;
   p.stages = stages;
   p.nhist = nhist;
   const size_t smem = need(nhist);

@@ -14,8 +14,12 @@ k = rsr.optimal_k_rsrpp(n)
 g = torch.Generator(device="cuda").manual_seed(0)
 A = (torch.randint(0, 3, (n, m), device="cuda", dtype=torch.int8, generator=g) - 1).to(torch.int8)
 idx = rsr.preprocess_ternary(A, k)
-v = torch.randint(-100, 101, (n,), device="cuda", generator=g).to(torch.int32)
-out = torch.empty(m, dtype=torch.int32, device="cuda")
+if os.environ.get("TRACE_F32"):  # fp32 activations: the fixed-point (FX) instance
+    v = torch.randn(n, device="cuda", generator=g)
+    out = torch.empty(m, dtype=torch.float32, device="cuda")
+else:
+    v = torch.randint(-100, 101, (n,), device="cuda", generator=g).to(torch.int32)
+    out = torch.empty(m, dtype=torch.int32, device="cuda")
 for _ in range(3):
     K._multiply_device(v, idx, True, None, out)
 torch.cuda.synchronize()
