@@ -38,7 +38,11 @@ namespace {
 constexpr int kScatterR = RSR_R;  // rows per scatter thread (multiple of 8)
 // scatter threads of a full CTA: kScatterR rows each, >= 16384 rows per CTA
 constexpr int kScatterThreads = (16384 / kScatterR + 31) / 32 * 32;
-constexpr int kFoldWarps = 4;  // dedicated fold warps per CTA
+#ifndef RSR_FW
+#define RSR_FW 4
+#endif
+constexpr int kFoldWarps = RSR_FW;  // dedicated fold warps per CTA (full CTAs); 8 measured 9% slower
+                                    // (80 registers, fold warps compete for issue and smem)
 constexpr int kMaxK = 16;
 #ifndef RSR_KA
 #define RSR_KA 1
@@ -173,8 +177,8 @@ __device__ __forceinline__ double pow2d(int e) {  // 2^e for |e| <= 1022
 // 2 = scheduled word-index codes (k = 12, 13; see common.cuh encode_key)
 template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, int CODES, int FW>
 __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
-  static_assert(FW == 1 || FW == 2 || FW == 4, "fold warps");
-  constexpr int FB = FW == 4 ? 2 : FW == 2 ? 1 : 0;  // key bits spanned by the fold warps
+  static_assert(FW == 1 || FW == 2 || FW == 4 || FW == 8, "fold warps");
+  constexpr int FB = FW == 8 ? 3 : FW == 4 ? 2 : FW == 2 ? 1 : 0;  // key bits spanned by the fold warps
   static_assert(R % 8 == 0 && R * kScatterThreads <= 32768, "rows per CTA");
   constexpr int LIMBS = FX ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem[];
