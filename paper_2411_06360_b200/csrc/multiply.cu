@@ -947,7 +947,9 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   // thread under the launch bounds)
   // small CTAs run one fold warp so that 4 of them share an SM — when that puts every block in
   // flight at once (with several blocks per CTA the single fold warp is the slower choice)
-  const int fw = (threads <= 128 && d.k <= 13 && (b1 - b0) <= 4 * device_sm_count()) ? 1 : kFoldWarps;
+  // (threads < 128: one fold warp always, so that FW = 4 means 4, 8 or 16 scatter warps and
+  // the fold warps form one aligned warpgroup)
+  const int fw = (threads < 128 || (threads == 128 && d.k <= 13 && (b1 - b0) <= 4 * device_sm_count())) ? 1 : kFoldWarps;
   const int cta_threads = threads + 32 * fw;
   const int per_sm = std::max<int>(1, (int)std::min<size_t>(std::min(2048 / cta_threads, 65536 / (cta_threads * 96)),
                                                             (228u << 10) / (smem + 1024)));
