@@ -186,15 +186,20 @@ class _HostPlan:
     """One host-buffer session (rsr_host_session_*: pinned staging, device scratch, mapped
     result + completion flag) for one index, vector type and thread, created on first use and
     destroyed with the index or the thread."""
-    __slots__ = ("session", "cols", "call", "__weakref__")
+    __slots__ = ("session", "cols", "call", "stream", "__weakref__")
 
     def __init__(self, idx, kind):
+        import torch
         L = _native.lib()
         h = ctypes.c_void_p()
         _native.check(L.rsr_host_session_create(ctypes.byref(idx.desc), _KIND_CODE[kind], ctypes.byref(h)))
         self.session = h.value
         self.cols = idx.cols
         self.call = _native.host_ext().multiply
+        # torch's current stream on the session's device, queried per call (sub-microsecond)
+        dev = torch.cuda.current_device()
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        self.stream = (lambda: raw(dev)) if raw is not None else _native.current_stream_ptr
         weakref.finalize(self, L.rsr_host_session_destroy, h.value)
 
 
@@ -217,7 +222,7 @@ def _run_host(idx, kind, v: np.ndarray, use_fold: bool) -> np.ndarray:
     plan = _host_plan(idx, kind)
     out = np.empty(plan.cols, np.float64)
     st = plan.call(plan.session, v, out, _native.F64, _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR,
-                   _native.current_stream_ptr())
+                   plan.stream())
     if st:
         _native.check(st)
     return out
@@ -253,7 +258,9 @@ def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray
             raise ValueError("vector must be 1-D with at least one entry")
         if raw.shape[0] != idx.rows:
             raise ValueError(f"vector length {raw.shape[0]} does not match {idx.rows} rows")
-        if raw.dtype.itemsize < 4 or raw.dtype == np.int32 or (raw.min() >= -2 ** 31 and raw.max() < 2 ** 31):
+        if raw.dtype == np.int32:
+            return _run_host(idx, "i32", raw if raw.flags.c_contiguous else np.ascontiguousarray(raw), use_fold)
+        if raw.dtype.itemsize < 4 or (raw.min() >= -2 ** 31 and raw.max() < 2 ** 31):
             return _run_host(idx, "i32", np.ascontiguousarray(raw, np.int32), use_fold)
         if compute == "int32":
             raise ValueError("integer activations exceed the int32 range")
@@ -282,6 +289,8 @@ def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray
 
 
 def _is_device_tensor(v) -> bool:
+    if type(v) is np.ndarray:  # the common host case, without touching torch
+        return False
     try:
         import torch
     except ImportError:  # pragma: no cover
