@@ -19,6 +19,10 @@ matrix), multiplies it, and the output slices are NCCL all-gathered every step
 (the north star's column-block sharding + all-gather).  value = N shard-matvecs
 per step / max-over-ranks time.
 
+--config ternary65536s (BASELINE config 5, strong scaling): ONE 65536 x 65536 matrix whose
+column blocks are split over the ranks (the multiply_parallel partition), padded slices
+all-gathered every step; value = full matvecs per second.
+
 --impl reference: the reference algorithm's CPU path (oracle/rsr_oracle.c, a C
 port of `_run_blocks` + `multiply_parallel`; the reference itself is Python +
 Numba and cannot travel to the GPU box) on all host cores.
@@ -50,7 +54,10 @@ CONFIGS = {
     "ternary65536": ("ternary", 65536, 65536, "ternary 65536x65536 RSR++ matvec, k=13"),
     "ternary16384b64": ("ternary", 16384, 16384, "ternary 16384x16384 RSR++, batch of 64 int32 activation vectors"),
     "ternary4096f32": ("ternary", 4096, 4096, "ternary 4096x4096 RSR++ matvec, k=9, single fp32 vector"),
+    "ternary65536s": ("ternary", 65536, 65536, "ternary 65536x65536 RSR++ matvec, k=13, column blocks sharded "
+                      "across the ranks (kernels.py:222 partition) + NCCL all-gather of the output"),
 }
+STRONG = {"ternary65536s"}  # BASELINE config 5: one matrix split over the ranks (strong scaling)
 FP32 = {"ternary4096f32"}
 FP32_TOL = 1e-5  # north star: fp32 activations within 1e-5 relative (norm-wise) of the fp64 reference
 BATCH = {"ternary16384b64": 64}
@@ -249,8 +256,20 @@ def run_ours(args, cfg):
     domain, n, m, desc = cfg
     k = rsr.optimal_k_rsrpp(n)
 
-    # ---- data: rank g's shard = columns [g*m, (g+1)*m) of the n x (N*m) matrix
-    A = make_matrix(domain, n, m, seed=rank)
+    # ---- data.  weak (default): rank g's shard = columns [g*m, (g+1)*m) of an n x (N*m) matrix.
+    # strong (BASELINE config 5): rank g owns the column blocks [g*NB//N, (g+1)*NB//N) of ONE
+    # n x m matrix (dist.shard_columns, the multiply_parallel partition), seeded by its first column
+    strong = args.config in STRONG
+    m_full = m
+    c0, c1 = (0, m)
+    if strong:
+        from paper_2411_06360_b200 import dist as D
+        c0, c1 = D.shard_columns(m, k, world, rank)
+        pad = max(D.slice_lengths(m, k, world))
+        m = c1 - c0
+    else:
+        pad = m
+    A = make_matrix(domain, n, m, seed=c0 if strong else rank)
     fp32 = args.config in FP32
     v = (np.random.default_rng([0, n, 2]).standard_normal(n).astype(np.float32) if fp32 else make_vector(n))
     dA = torch.from_numpy(A).cuda()
@@ -322,16 +341,17 @@ def run_ours(args, cfg):
 
     stream = torch.cuda.current_stream()
     odt = torch.float32 if fp32 else torch.int32
-    out = torch.empty(m, dtype=odt, device="cuda")
+    out_pad = torch.zeros(pad, dtype=odt, device="cuda")  # equal all-gather sizes (strong: slices differ)
+    out = out_pad[:m]
     mult = rsr.multiply_ternary if domain == "ternary" else rsr.multiply_rsr
-    gathered = torch.empty(world * m, dtype=odt, device="cuda") if world > 1 else None
+    gathered = torch.empty(world * pad, dtype=odt, device="cuda") if world > 1 else None
 
     from paper_2411_06360_b200 import kernels as K
 
     def step(i):
         K._multiply_device(dv, copies[i % ncopies], True, None, out)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, out)
+            dist.all_gather_into_tensor(gathered, out_pad)
 
     for i in range(max(args.warmup, 3)):
         step(i)
@@ -347,7 +367,7 @@ def run_ours(args, cfg):
             for i in range(args.steps):
                 K._multiply_device(dv, copies[i % ncopies], True, None, out)
                 if world > 1:
-                    dist.all_gather_into_tensor(gathered, out)
+                    dist.all_gather_into_tensor(gathered, out_pad)
     stream.wait_stream(cap)
     graph.replay()  # warm the graph itself
     torch.cuda.synchronize()
@@ -393,7 +413,8 @@ def run_ours(args, cfg):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
     ms_per_step = total_ms / args.steps
-    value = world * 1e3 / ms_per_step  # shard-matvecs (16384^2-equivalents) per second
+    # weak: shard-matvecs per second (N shards per step); strong: full matvecs per second
+    value = (1 if strong else world) * 1e3 / ms_per_step
 
     # ---- e2e through the reference-facing API with host buffers (rank-local)
     v_host = v.copy()
@@ -451,14 +472,15 @@ def run_ours(args, cfg):
     line = {
         "metric": "ternary RSR++ matvec vectors/sec" if domain == "ternary" else "binary RSR++ matvec vectors/sec",
         "value": value, "unit": "vectors/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if fp32 else "int32", "data": "synthetic",
-        "config": {"workload": desc + (f"; {world} column shards + NCCL all-gather" if world > 1 else ""),
-                   "n": n, "m": m, "k": k, "batch": 1, "l2": f"rotating {ncopies} index copies (>= 4x L2)",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f32" if fp32 else "int32", "data": "synthetic",
+        "config": {"workload": desc + (f"; {world} column shards + NCCL all-gather" if world > 1 and not strong else ""),
+                   "n": n, "m": m_full, "k": k, "batch": 1, "l2": f"rotating {ncopies} index copies (>= 4x L2)",
+                   **({"shard_cols": [c0, c1], "ranks": world} if strong else {}),
                    "form": "scatter (fp32: exact two-limb fixed point)" if fp32 else "scatter",
                    "preprocess_s": round(preprocess_s, 4)},
         "gpu_launches": args.steps * (1 if idx.desc.rows <= 16384 else 2),
-        "e2e": {"value": world * 1e3 / e2e_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * n,
+        "e2e": {"value": (1 if strong else world) * 1e3 / e2e_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * n,
                 "d2h_bytes_per_step": (4 if fp32 else 8) * m,
                 "path": f"rsr.multiply_ternary(numpy {'float32' if fp32 else 'int32'} v, idx)"
                         + (" on every rank's shard (no collective: each rank's slice returns to its host)"
