@@ -211,8 +211,10 @@ rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_d
   if (loop) {  // one multiply per vector
     const size_t vsz = v_dtype == RSR_F64 ? 8 : 4, osz = out_dtype == RSR_F64 ? 8 : 4;
     for (int64_t i = 0; i < batch; ++i) {
+      // vector i > 0 depends only on what vector 0's launch already waited for: its launch
+      // overlaps the previous vector's tail (distinct V row and OUT row)
       st = multiply(*desc, (const char*)V + i * desc->rows * vsz, v_dtype, (char*)OUT + i * desc->cols * osz, out_dtype,
-                    variant, RSR_FORM_AUTO, 0, desc->nblocks, (cudaStream_t)stream);
+                    variant, RSR_FORM_AUTO, 0, desc->nblocks, (cudaStream_t)stream, nullptr, nullptr, i > 0);
       if (st != RSR_OK) return st;
     }
     return RSR_OK;

@@ -167,8 +167,11 @@ struct Publish {
 // multiply.cu: one fused multiply over blocks [b0, b1).  With `pub`, a single-split scatter
 // launch with int32 / fp32 results also publishes them (then *published = true); otherwise the
 // caller copies the results back.
+// `independent`: this launch reads nothing the previous launch in the stream writes and writes
+// nothing it touches (e.g. vector i > 0 of a batch), so the scatter kernel skips its grid
+// dependency wait and overlaps the previous launch's tail.
 rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
                     rsr_form form, int b0, int b1, cudaStream_t s, const Publish* pub = nullptr,
-                    bool* published = nullptr);
+                    bool* published = nullptr, bool independent = false);
 
 }  // namespace rsr

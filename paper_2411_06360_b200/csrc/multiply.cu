@@ -113,6 +113,7 @@ struct ScatterParams {
   int codes;          // code format: 0 byte offsets in row order, 1 scheduled byte offsets, 2 scheduled word indices
   uint32_t code_mask; // mask of the group's first two code words (clears the control bits)
   Publish pub;        // host_out != nullptr: also store the results into mapped host memory + flag
+  int independent;    // no data dependence on the previous launch: skip the grid dependency wait
 };
 
 // Logical-order view of one int4 of swizzled bins: element e of the result is logical bin
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   }
   for (int i = t; i < hist_words / 4; i += blockDim.x) reinterpret_cast<int4*>(hist)[i] = make_int4(0, 0, 0, 0);
   // v and out may belong to the previous kernel in the stream: wait for it here (PDL)
-  grid_dependency_wait();
+  if (!p.independent) grid_dependency_wait();
   if (!p.atomic_out)  // a single-split launch owns its output columns
     for (int i = t; i < nunits * p.k; i += blockDim.x) {
       const int b = p.b_begin + col_cta + (i / p.k) * ncol;
@@ -895,9 +896,10 @@ rsr_status launch_scatter_fw(const ScatterParams& p, int grid, size_t smem, int 
 }
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, void* out, rsr_dtype out_dtype, bool pp,
-                            int b0, int b1, cudaStream_t s, const Publish* pub, bool* published) {
+                            int b0, int b1, cudaStream_t s, const Publish* pub, bool* published, bool independent) {
   if (d.k > 14) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply supports k <= 14");
   ScatterParams p{};
+  p.independent = independent ? 1 : 0;
   const bool publish = pub && out_dtype != RSR_F64;  // single split only (decided below)
   for (int h = 0; h < d.halves; ++h) p.key[h] = d.half[h].bucket;
   p.v = reinterpret_cast<const int32_t*>(v);
@@ -1018,7 +1020,8 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
 }  // namespace
 
 rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
-                    rsr_form form, int b0, int b1, cudaStream_t s, const Publish* pub, bool* published) {
+                    rsr_form form, int b0, int b1, cudaStream_t s, const Publish* pub, bool* published,
+                    bool independent) {
   const bool pp = var == RSR_VARIANT_RSRPP;
   if (published) *published = false;
   if (b0 >= b1) return RSR_OK;
@@ -1029,11 +1032,11 @@ rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* 
   if (form == RSR_FORM_SCATTER) {
     if (vt == RSR_F32) {
       if (!fx_ok) return fail(RSR_ERR_INVALID, "fp32 scatter form needs rows <= 16384, k <= 14, fp32 output");
-      return multiply_scatter(d, v, true, out, ot, pp, b0, b1, s, pub, published);
+      return multiply_scatter(d, v, true, out, ot, pp, b0, b1, s, pub, published, independent);
     }
     if (vt != RSR_I32) return fail(RSR_ERR_INVALID, "scatter form needs int32 or fp32 activations");
     if (ot != RSR_I32 && ot != RSR_F64) return fail(RSR_ERR_INVALID, "int32 activations produce int32 or float64");
-    return multiply_scatter(d, v, false, out, ot, pp, b0, b1, s, pub, published);
+    return multiply_scatter(d, v, false, out, ot, pp, b0, b1, s, pub, published, independent);
   }
   if (vt != ot) return fail(RSR_ERR_INVALID, "gather form writes the activation dtype");
   switch (vt) {
