@@ -32,6 +32,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import os
 import statistics
 import subprocess
@@ -211,7 +212,7 @@ def run_reference(args, cfg):
         return
     domain, n, m, desc = cfg
     from paper_2411_06360_b200.indexer import optimal_k_rsrpp
-    k = optimal_k_rsrpp(n)
+    k = args.k or optimal_k_rsrpp(n)
     A = make_matrix(domain, n, m)
     v = (np.random.default_rng([0, n, 2]).standard_normal(n).astype(np.float32) if args.config in FP32
          else make_vector(n))
@@ -254,7 +255,11 @@ def run_ours(args, cfg):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     domain, n, m, desc = cfg
-    k = rsr.optimal_k_rsrpp(n)
+    # block width: the B200 tuner (indexer.optimal_k_b200, measured per shape) unless --k; the
+    # CPU legs run the reference's own tuner (optimal_k_rsrpp), as the reference does
+    k_ref = rsr.optimal_k_rsrpp(n)
+    k = args.k or rsr.optimal_k_b200(n, m)
+    desc = re.sub(r"k=\d+", f"k={k}", desc)
 
     # ---- data.  weak (default): rank g's shard = columns [g*m, (g+1)*m) of an n x (N*m) matrix.
     # strong (BASELINE config 5): rank g owns the column blocks [g*NB//N, (g+1)*NB//N) of ONE
@@ -475,7 +480,8 @@ def run_ours(args, cfg):
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "f32" if fp32 else "int32", "data": "synthetic",
         "config": {"workload": desc + (f"; {world} column shards + NCCL all-gather" if world > 1 and not strong else ""),
-                   "n": n, "m": m_full, "k": k, "batch": 1, "l2": f"rotating {ncopies} index copies (>= 4x L2)",
+                   "n": n, "m": m_full, "k": k, "k_tuner": "optimal_k_b200 (reference tuner: k=%d)" % k_ref,
+                   "batch": 1, "l2": f"rotating {ncopies} index copies (>= 4x L2)",
                    **({"shard_cols": [c0, c1], "ranks": world} if strong else {}),
                    "form": "scatter (fp32: exact two-limb fixed point)" if fp32 else "scatter",
                    "preprocess_s": round(preprocess_s, 4)},
@@ -496,12 +502,12 @@ def run_ours(args, cfg):
     if gpu_standard is not None:
         line["gpu_standard"] = gpu_standard
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu_s, reps, workers, _ = time_cpu_reference(make_matrix(domain, n, m), v, k, domain,
+        cpu_s, reps, workers, _ = time_cpu_reference(make_matrix(domain, n, m), v, k_ref, domain,
                                                      min_seconds=args.cpu_seconds)
         line["cpu_baseline"] = {"value": 1.0 / cpu_s, "unit": "vectors/s", "cores": workers, "kind": "port",
                                 "sample": f"{reps} full {n}x{m} RSR++ matvecs, fp64, C port of "
                                           "kernels.py:127-239 on {workers} threads".replace("{workers}", str(workers))}
-        line["cpu_baseline"].update(time_cpu_extras(make_matrix(domain, n, m), v, k, domain))
+        line["cpu_baseline"].update(time_cpu_extras(make_matrix(domain, n, m), v, k_ref, domain))
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -591,6 +597,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="ternary16384", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--k", type=int, default=0, help="block width override (default: the reference tuner)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

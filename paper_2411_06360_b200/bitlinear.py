@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 
 from .core import TernaryMatrix
-from .indexer import optimal_k_rsrpp, preprocess_ternary
+from .indexer import optimal_k_b200, preprocess_ternary
 from .kernels import multiply_batched, multiply_ternary
 
 
@@ -26,7 +26,7 @@ class BitLinear(_torch().nn.Module):
     """y = x · W (+ scale) with W ternary [in_features, out_features] held as an RSR index.
 
     weight: int8 CUDA tensor / NumPy array / TernaryMatrix with entries in {-1, 0, 1}.
-    k: block width (default: the reference tuner, optimal_k_rsrpp(in_features)).
+    k: block width (default: the B200 tuner, optimal_k_b200(in_features, out_features)).
     scale: optional float or [out_features] tensor multiplied into the output.
     """
 
@@ -38,7 +38,7 @@ class BitLinear(_torch().nn.Module):
         else:
             rows, cols = weight.shape
         self.in_features, self.out_features = int(rows), int(cols)
-        self.k = int(k) if k is not None else optimal_k_rsrpp(self.in_features)
+        self.k = int(k) if k is not None else optimal_k_b200(self.in_features, self.out_features)
         self.variant = variant
         if isinstance(weight, np.ndarray):
             weight = TernaryMatrix(weight.astype(np.int8))

@@ -148,3 +148,12 @@ def test_butterfly_schedule_roundtrip():
         slots[..., j] |= ((c >> (3 * j)) & 7) << 13
     back = unschedule_codes(slots.reshape(nb, rs).astype(np.uint16), k)
     assert np.array_equal(back, codes.astype(np.uint16))
+
+
+def test_b200_tuner_is_valid_for_every_row_count(rsr):
+    """optimal_k_b200 (the device cost model) always returns a k the index accepts."""
+    from paper_2411_06360_b200.indexer import max_k_for_rows
+    for rows in (1, 2, 3, 6, 64, 1000, 4096, 14336, 16384, 65536, 1 << 20):
+        k = rsr.optimal_k_b200(rows, 4096)
+        assert 1 <= k <= max(1, max_k_for_rows(rows)) and k <= 16
+    assert rsr.optimal_k_b200(16384, 16384) == rsr.optimal_k_rsrpp(16384) == 11  # headline unchanged
