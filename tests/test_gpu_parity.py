@@ -368,7 +368,7 @@ def test_bitlinear_decode_chain_graph(rsr, cuda):
     Wd = rng.integers(-1, 2, size=(14336, 4096), dtype=np.int8)
     up = rsr.BitLinear(torch.from_numpy(Wu).cuda())
     down = rsr.BitLinear(torch.from_numpy(Wd).cuda())
-    assert (up.k, down.k) == (rsr.optimal_k_rsrpp(4096), rsr.optimal_k_rsrpp(14336))
+    assert (up.k, down.k) == (rsr.optimal_k_b200(4096, 14336), rsr.optimal_k_b200(14336, 4096))
     x = torch.from_numpy(rng.standard_normal(4096).astype(np.float32)).cuda()
     y = down(up(x) * 0.01)
     h = (x.cpu().double().numpy() @ Wu.astype(np.float64)).astype(np.float32).astype(np.float64) * 0.01
