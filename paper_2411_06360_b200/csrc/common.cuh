@@ -153,15 +153,20 @@ __host__ __device__ __forceinline__ int block_width(int64_t cols, int k, int b) 
 }
 
 // Result publishing for host-buffer sessions (csrc/host.cu): a single-split scatter multiply
-// also delivers its results to the host.  Every CTA stores its final columns into MAPPED host
-// memory and arrives on a device counter (gpu-scope release); the last arrival fences at system
-// scope and raises a host-visible flag.  The host polls the flag instead of copying back and
-// synchronizing the stream (tools/microbench/sync_probe.cu, session_timeline.cu).
+// also delivers its results into MAPPED host memory, in one of two ways
+// (tools/microbench/session_timeline.cu measured both):
+//  * tagged (tagged != nullptr): each result is one 64-bit store (seq << 32 | value), single-copy
+//    atomic, and the host accepts a word once its tag is the call's seq.  No fence, counter or
+//    flag, but the host reads 8 bytes per result: the faster scheme up to ~8 K columns.
+//  * flagged (host_out != nullptr): each CTA stores its 4-byte results, one thread releases them
+//    at gpu scope and arrives on a device counter, and the last arrival fences at system scope
+//    (~3 us) and raises the flag the host polls.  4 bytes per result on the host side.
 struct Publish {
-  void* host_out;     // device pointer of the mapped result buffer [cols], 4-byte elements
-  uint32_t* counter;  // device, 0 between calls
-  uint32_t* flag;     // device pointer of the mapped flag word
-  uint32_t seq;       // value the flag receives
+  unsigned long long* tagged;  // device pointer of the mapped tagged-result buffer [cols]
+  void* host_out;              // device pointer of the mapped result buffer [cols], 4-byte elements
+  uint32_t* counter;           // device, 0 between calls (flagged)
+  uint32_t* flag;              // device pointer of the mapped flag word (flagged)
+  uint32_t seq;                // tag / flag value of this call (never 0)
 };
 
 // multiply.cu: one fused multiply over blocks [b0, b1).  With `pub`, a single-split scatter

@@ -2,14 +2,15 @@
 // (`multiply_ternary(numpy v, idx)`, kernels.py:196-206 — host vector in, fresh host result out).
 //
 // A session owns, for one index and one vector type, pinned staging for v, a device copy of v
-// and of the result, a MAPPED pinned result buffer and a mapped completion flag, allocated once
-// and reused every call.  A call is: memcpy v -> pinned staging, H2D(v), the multiply, and the
-// conversion into the caller's buffer.  A single-split scatter multiply (int32 / fp32
-// activations, rows <= 16384) publishes its results itself (csrc/multiply.cu, Publish: every
-// CTA stores its columns into the mapped buffer, the last one raises the flag), and the host
-// polls the flag — no D2H copy and no stream synchronize between the kernel and the caller
-// (tools/microbench/sync_probe.cu, session_timeline.cu measured the completion schemes on the
-// B200 box).  Other forms are followed by a D2H copy and a stream synchronize.
+// and of the result, and mapped pinned result memory, allocated once and reused every call.
+// A call is: memcpy v -> pinned staging, H2D(v), the multiply, and the conversion into the
+// caller's buffer.  A single-split scatter multiply (int32 / fp32 activations, rows <= 16384)
+// publishes its results into the mapped memory itself (csrc/common.cuh Publish: seq-tagged
+// 64-bit words up to 8 K columns, 4-byte results + a fenced completion flag beyond), so no D2H
+// copy and no stream synchronize sit between the kernel and the caller
+// (tools/microbench/sync_probe.cu, session_timeline.cu measured the alternatives on the B200
+// box).  Other forms are followed by a D2H copy and a stream synchronize.
+#include <emmintrin.h>
 #include <immintrin.h>
 
 #include <atomic>
@@ -31,14 +32,17 @@ struct rsr_host_session {
   rsr_index_desc desc;
   rsr_dtype v_dtype;        // host vector type = device result type (int32 -> int32, fp32 -> fp32, fp64 -> fp64)
   void* h_v = nullptr;      // pinned staging [rows]
-  void* h_res = nullptr;    // pinned, mapped [cols] of v_dtype (published results)
+  bool tagged = false;                      // publish mode (see rsr::Publish)
+  unsigned long long* h_tag = nullptr;      // pinned, mapped [cols] tagged results (seq << 32 | value)
+  unsigned long long* h_tag_dev = nullptr;
+  void* h_res = nullptr;                    // pinned, mapped [cols] 4-byte results (flagged)
   void* h_res_dev = nullptr;
-  void* h_copy = nullptr;   // pinned [cols] of v_dtype (D2H path)
-  uint32_t* h_flag = nullptr;  // pinned, mapped
+  uint32_t* h_flag = nullptr;               // pinned, mapped (flagged)
   uint32_t* h_flag_dev = nullptr;
+  uint32_t* d_counter = nullptr;
+  void* h_copy = nullptr;   // pinned [cols] of v_dtype (D2H path)
   void* d_v = nullptr;
   void* d_out = nullptr;
-  uint32_t* d_counter = nullptr;
   uint32_t seq = 0;
 };
 
@@ -49,10 +53,11 @@ namespace {
 void session_free(rsr_host_session* h) {
   if (!h) return;
   if (h->h_v) cudaFreeHost(h->h_v);
+  if (h->h_tag) cudaFreeHost(h->h_tag);
   if (h->h_res) cudaFreeHost(h->h_res);
-  if (h->h_copy) cudaFreeHost(h->h_copy);
   if (h->h_flag) cudaFreeHost(h->h_flag);
   if (h->d_counter) cudaFree(h->d_counter);
+  if (h->h_copy) cudaFreeHost(h->h_copy);
   if (h->d_v) cudaFree(h->d_v);
   if (h->d_out) cudaFree(h->d_out);
   delete h;
@@ -97,20 +102,30 @@ rsr_status rsr_host_session_create(const rsr_index_desc* desc, rsr_dtype v_dtype
   const size_t vb = rsr::dsize(v_dtype) * (size_t)desc->rows;
   const size_t ob = rsr::dsize(v_dtype) * (size_t)desc->cols;
   rsr_status st = cuda_check(cudaHostAlloc(&h->h_v, vb, cudaHostAllocDefault), "session pinned v");
-  if (st == RSR_OK) st = cuda_check(cudaHostAlloc(&h->h_res, ob, cudaHostAllocMapped), "session mapped result");
-  if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer(&h->h_res_dev, h->h_res, 0), "session result mapping");
+  // tagged words up to 8 K columns, the fenced flag beyond (the host reads 8 vs 4 bytes per
+  // result against a ~4 us fence + arrival; session_timeline.cu / e2e probes)
+  h->tagged = desc->cols <= 8192;
+  if (h->tagged) {
+    if (st == RSR_OK)
+      st = cuda_check(cudaHostAlloc((void**)&h->h_tag, 8 * (size_t)desc->cols, cudaHostAllocMapped), "session mapped result");
+    if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer((void**)&h->h_tag_dev, h->h_tag, 0), "session result mapping");
+    if (st == RSR_OK) std::memset(h->h_tag, 0, 8 * (size_t)desc->cols);  // tag 0: no call's result
+  } else {
+    if (st == RSR_OK) st = cuda_check(cudaHostAlloc(&h->h_res, ob, cudaHostAllocMapped), "session mapped result");
+    if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer(&h->h_res_dev, h->h_res, 0), "session result mapping");
+    if (st == RSR_OK) st = cuda_check(cudaHostAlloc((void**)&h->h_flag, 64, cudaHostAllocMapped), "session flag");
+    if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer((void**)&h->h_flag_dev, h->h_flag, 0), "session flag mapping");
+    if (st == RSR_OK) st = cuda_check(cudaMalloc((void**)&h->d_counter, 64), "session counter");
+    if (st == RSR_OK) st = cuda_check(cudaMemset(h->d_counter, 0, 64), "session counter init");
+    if (st == RSR_OK) *h->h_flag = 0;
+  }
   if (st == RSR_OK) st = cuda_check(cudaHostAlloc(&h->h_copy, ob, cudaHostAllocDefault), "session pinned result");
-  if (st == RSR_OK) st = cuda_check(cudaHostAlloc((void**)&h->h_flag, 64, cudaHostAllocMapped), "session flag");
-  if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer((void**)&h->h_flag_dev, h->h_flag, 0), "session flag mapping");
-  if (st == RSR_OK) st = cuda_check(cudaMalloc((void**)&h->d_counter, 64), "session counter");
-  if (st == RSR_OK) st = cuda_check(cudaMemset(h->d_counter, 0, 64), "session counter init");
   if (st == RSR_OK) st = cuda_check(cudaMalloc(&h->d_v, vb), "session device v");
   if (st == RSR_OK) st = cuda_check(cudaMalloc(&h->d_out, ob), "session device result");
   if (st != RSR_OK) {
     session_free(h);
     return st;
   }
-  *h->h_flag = 0;
   *out = h;
   return RSR_OK;
 }
@@ -135,8 +150,9 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, si
   if (tr) { t1 = now_us(); g_trace.v[0].push_back(t1 - t0); t0 = t1; }
   rsr_status st = cuda_check(cudaMemcpyAsync(h->d_v, h->h_v, vb, cudaMemcpyHostToDevice, s), "H2D v");
   if (st != RSR_OK) return st;
-  const uint32_t seq = ++h->seq == 0 ? ++h->seq : h->seq;  // never 0 (the flag's initial value)
-  const rsr::Publish pub{h->h_res_dev, h->d_counter, h->h_flag_dev, seq};
+  const uint32_t seq = ++h->seq == 0 ? ++h->seq : h->seq;  // never 0 (the buffer's initial tag)
+  const rsr::Publish pub = h->tagged ? rsr::Publish{h->h_tag_dev, nullptr, nullptr, nullptr, seq}
+                                     : rsr::Publish{nullptr, h->h_res_dev, h->d_counter, h->h_flag_dev, seq};
   bool published = false;
   st = rsr::multiply(d, h->d_v, h->v_dtype, h->d_out, h->v_dtype, variant, RSR_FORM_AUTO, 0, d.nblocks, s, &pub,
                      &published);
@@ -144,8 +160,10 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, si
   if (!published && (st = cuda_check(cudaMemcpyAsync(h->h_copy, h->d_out, ob, cudaMemcpyDeviceToHost, s), "D2H out")) != RSR_OK)
     return st;
   if (tr) { t1 = now_us(); g_trace.v[1].push_back(t1 - t0); t0 = t1; }
-  if (published) {
-    // poll the flag; every few thousand polls ask the stream whether it failed
+  if (!published && (st = cuda_check(cudaStreamSynchronize(s), "stream sync")) != RSR_OK) return st;
+  if (tr) { t1 = now_us(); g_trace.v[2].push_back(t1 - t0); t0 = t1; }
+  if (published && !h->tagged) {
+    // flagged: poll the flag; every few thousand polls ask the stream whether it failed
     volatile uint32_t* flag = h->h_flag;
     for (uint32_t spins = 1; *flag != seq; ++spins) {
       _mm_pause();
@@ -159,14 +177,62 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, si
       }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
-  } else if ((st = cuda_check(cudaStreamSynchronize(s), "stream sync")) != RSR_OK) {
-    return st;
   }
-  if (tr) { t1 = now_us(); g_trace.v[2].push_back(t1 - t0); t0 = t1; }
-  const void* res = published ? h->h_res : h->h_copy;
-  if (out_dtype == h->v_dtype) std::memcpy(out_host, res, ob);
-  else if (h->v_dtype == RSR_I32) convert((const int32_t*)res, (double*)out_host, d.cols);
-  else convert((const float*)res, (double*)out_host, d.cols);
+  if (published && h->tagged) {
+    // every word is accepted once its tag is this call's seq (an aligned 16-byte load sees two
+    // whole 64-bit stores); two words per step, SSE2: the tag check, the int32 / fp32 -> fp64
+    // conversion and the store.  While a pair is not ready, spin (asking the stream every few
+    // thousand polls whether the launch failed).
+    const int64_t m = d.cols;
+    const unsigned long long* res = h->h_tag;
+    const __m128i want = _mm_set1_epi32((int)seq);
+    const bool f64 = out_dtype == RSR_F64, i32 = h->v_dtype == RSR_I32;
+    auto wait_ready = [&](int64_t i, int64_t n) -> rsr_status {  // words [i, i + n) tagged
+      for (uint32_t spins = 1;; ++spins) {
+        asm volatile("" ::: "memory");
+        bool ok = true;
+        for (int64_t j = i; j < i + n; ++j) ok &= (uint32_t)(((const volatile unsigned long long*)res)[j] >> 32) == seq;
+        if (ok) return RSR_OK;
+        _mm_pause();
+        if ((spins & 1023u) == 0) {
+          const cudaError_t e = cudaStreamQuery(s);
+          if (e == cudaSuccess) {
+            asm volatile("" ::: "memory");
+            bool done = true;
+            for (int64_t j = i; j < i + n; ++j) done &= (uint32_t)(((const volatile unsigned long long*)res)[j] >> 32) == seq;
+            if (!done) return fail(RSR_ERR_CUDA, "host session: the multiply completed without publishing");
+          } else if (e != cudaErrorNotReady) {
+            return cuda_check(e, "host session multiply");
+          }
+        }
+      }
+    };
+    int64_t i = 0;
+    while (i + 2 <= m) {
+      asm volatile("" ::: "memory");
+      const __m128i x = _mm_load_si128(reinterpret_cast<const __m128i*>(res + i));
+      const __m128i tags = _mm_shuffle_epi32(x, _MM_SHUFFLE(3, 1, 3, 1));
+      if ((_mm_movemask_epi8(_mm_cmpeq_epi32(tags, want)) & 0xff) != 0xff) {
+        if ((st = wait_ready(i, 2)) != RSR_OK) return st;
+        continue;  // reload the pair
+      }
+      const __m128i vals = _mm_shuffle_epi32(x, _MM_SHUFFLE(2, 0, 2, 0));
+      if (f64) _mm_storeu_pd((double*)out_host + i, i32 ? _mm_cvtepi32_pd(vals) : _mm_cvtps_pd(_mm_castsi128_ps(vals)));
+      else _mm_storel_epi64(reinterpret_cast<__m128i*>((uint32_t*)out_host + i), vals);
+      i += 2;
+    }
+    if (i < m) {
+      if ((st = wait_ready(i, 1)) != RSR_OK) return st;
+      const uint32_t bits = (uint32_t)((const volatile unsigned long long*)res)[i];
+      if (f64) ((double*)out_host)[i] = i32 ? (double)(int32_t)bits : (double)__builtin_bit_cast(float, bits);
+      else ((uint32_t*)out_host)[i] = bits;
+    }
+  } else {
+    const void* res = published ? h->h_res : h->h_copy;  // flagged publish, or the D2H copy
+    if (out_dtype == h->v_dtype) std::memcpy(out_host, res, ob);
+    else if (h->v_dtype == RSR_I32) convert((const int32_t*)res, (double*)out_host, d.cols);
+    else convert((const float*)res, (double*)out_host, d.cols);
+  }
   if (tr) g_trace.v[3].push_back(now_us() - t0);
   return RSR_OK;
 }

@@ -522,31 +522,38 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       if (fw == 0 && f < 40) TRACE(400 + f);
     }
     if (fw == 0) TRACE(6);
-    if (p.pub.host_out) {
-      // publish (host-buffer sessions; single split, so this CTA owns its columns): once every
-      // fold warp has added its share, the CTA's final columns go to mapped host memory (plain
-      // stores), then ONE thread releases them at gpu scope (fence after the barrier: cumulative
-      // over the CTA's stores) and arrives on the counter.  The grid's last arrival acquires
-      // every CTA's release, fences at system scope and raises the flag: host sees the flag =>
-      // host sees every CTA's stores (causality order), with one system fence per launch
-      // instead of one per CTA (tools/microbench/sync_probe.cu)
+    if (p.pub.tagged || p.pub.host_out) {
+      // publish (host-buffer sessions; single split, so this CTA owns its columns), once every
+      // fold warp has added its share (see Publish)
       const int ft = fw * 32 + lane;
-      uint32_t* hout = reinterpret_cast<uint32_t*>(p.pub.host_out);
       const uint32_t* dout = reinterpret_cast<const uint32_t*>(out);
-      __threadfence();  // my output reductions / stores are performed at L2
+      __threadfence();  // my output reductions / stores are performed at L2 before the barrier
       asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
+      if (fw == 0) TRACE(500);
+      const unsigned long long tag = (unsigned long long)p.pub.seq << 32;
+      uint32_t* hout = reinterpret_cast<uint32_t*>(p.pub.host_out);
       for (int i = ft; i < nunits * p.k; i += 32 * FW) {
         const int b = p.b_begin + col_cta + (i / p.k) * ncol;
         const int c = i % p.k;
-        if (c < block_width(p.cols, p.k, b)) hout[(int64_t)b * p.k + c] = __ldcg(dout + (int64_t)b * p.k + c);
+        if (c < block_width(p.cols, p.k, b)) {
+          const int64_t o = (int64_t)b * p.k + c;
+          const uint32_t val = __ldcg(dout + o);
+          if (p.pub.tagged) asm volatile("st.global.u64 [%0], %1;" ::"l"(p.pub.tagged + o), "l"(tag | val) : "memory");
+          else hout[o] = val;
+        }
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
-      if (ft == 0) {
-        __threadfence();
-        if (atomicAdd(p.pub.counter, 1u) == gridDim.x - 1) {
-          __threadfence_system();
-          *p.pub.counter = 0;  // ready for the next call (stream-ordered)
-          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pub.flag), "r"(p.pub.seq) : "memory");
+      if (fw == 0) TRACE(501);
+      if (!p.pub.tagged) {
+        // flagged: one gpu-scope release per CTA (after the barrier: cumulative over the CTA's
+        // stores), the last arrival acquires them all, fences at system scope, raises the flag
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
+        if (ft == 0) {
+          __threadfence();
+          if (atomicAdd(p.pub.counter, 1u) == gridDim.x - 1) {
+            __threadfence_system();
+            *p.pub.counter = 0;  // ready for the next call (stream-ordered)
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pub.flag), "r"(p.pub.seq) : "memory");
+          }
         }
       }
     }

@@ -431,8 +431,10 @@ def test_counted_twins_vs_reference(rsr, cuda):
 
 # ----------------------------------------------------------------------------- host-buffer sessions
 @pytest.mark.parametrize("rows,cols,k", [(1, 1, 1), (37, 29, 3), (1000, 777, 8), (16384, 1001, 11),
-                                         (20000, 515, 12)])
+                                         (20000, 515, 12), (2048, 8193, 10), (512, 12001, 9)])
 def test_host_session_all_types(rsr, cuda, rows, cols, k):
+    # (up to 8192 columns the kernel publishes seq-tagged words, beyond it a fenced flag;
+    # rows > 16384 take the D2H path)
     """NumPy in -> fresh fp64 NumPy out through the host session (H2D, multiply, publish into
     mapped memory, flag poll): int32 / int64 bit-exact, fp32 within the north-star bound, fp64
     within the reference's float tolerance; repeated calls reuse the session."""

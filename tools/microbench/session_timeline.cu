@@ -84,19 +84,25 @@ int main() {
   }
   cudaStreamSynchronize(s);
   std::vector<unsigned long long> tr(148 * 512);
-  std::vector<double> rows[8];
+  std::vector<double> rows[10];
   for (int it = 0; it < 200; ++it) {
     const double t0 = host_ns();
     CK(rsr_host_session_multiply(sess, v.data(), n * 4, out.data(), m * 8, RSR_F64, RSR_VARIANT_RSRPP, s));
     const double t1 = host_ns();
     CK(rsr_debug_trace_copy(tr.data(), tr.size()));
-    double cs = 1e300, ce = 0, fe = 0, pe = 0;
+    double cs = 1e300, ce = 0, fe = 0, pe = 0, p0 = 0, p1 = 0, p2 = 0, p3 = 0;
     for (int c = 0; c < 148; ++c) {
       cs = std::min(cs, (double)tr[c * 512 + 0]);
       pe = std::max(pe, (double)tr[c * 512 + 1]);
       ce = std::max(ce, (double)tr[c * 512 + 7]);
       fe = std::max(fe, (double)tr[c * 512 + 6]);
+      p0 = std::max(p0, (double)tr[c * 512 + 500]);
+      p1 = std::max(p1, (double)tr[c * 512 + 501]);
+      p2 = std::max(p2, (double)tr[c * 512 + 502]);
+      p3 = std::max(p3, (double)tr[c * 512 + 503]);
     }
+    const double flag_seen = t1 - t0;  // upper bound (includes the host conversion)
+    (void)flag_seen;
     if (it >= 20) {
       rows[0].push_back((t1 - t0) / 1e3);
       rows[1].push_back((cs + off - t0) / 1e3);
@@ -104,11 +110,16 @@ int main() {
       rows[3].push_back((ce + off - t0) / 1e3);
       rows[4].push_back((fe + off - t0) / 1e3);
       rows[5].push_back((fe - cs) / 1e3);
+      rows[6].push_back((p0 + off - t0) / 1e3);
+      rows[7].push_back((p1 + off - t0) / 1e3);
+      rows[8].push_back((p2 + off - t0) / 1e3);
+      rows[9].push_back((p3 + off - t0) / 1e3);
     }
   }
-  const char* names[6] = {"call total", "first CTA start", "last prologue end", "last scatter end", "last fold+publish end",
-                          "kernel span"};
-  for (int i = 0; i < 6; ++i) {
+  const char* names[10] = {"call total", "first CTA start", "last prologue end", "last scatter end", "last fold end",
+                           "kernel span", "publish: folds done (last CTA)", "publish: host stores issued",
+                           "publish: (unused)", "publish: (unused)"};
+  for (int i = 0; i < 10; ++i) {
     std::sort(rows[i].begin(), rows[i].end());
     printf("%-24s median %7.2f us  (p10 %7.2f  p90 %7.2f)\n", names[i], rows[i][rows[i].size() / 2],
            rows[i][rows[i].size() / 10], rows[i][rows[i].size() * 9 / 10]);
