@@ -487,7 +487,9 @@ def run_ours(args, cfg):
                    "preprocess_s": round(preprocess_s, 4)},
         "gpu_launches": args.steps * (1 if idx.desc.rows <= 16384 else 2),
         "e2e": {"value": (1 if strong else world) * 1e3 / e2e_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * n,
-                "d2h_bytes_per_step": (4 if fp32 else 8) * m,
+                # mapped result words the host reads (csrc/host.cu): 8-byte seq-tagged words up
+                # to 8 K columns, 4-byte results behind the fenced flag beyond
+                "d2h_bytes_per_step": (8 if m <= 8192 else 4) * m,
                 "path": f"rsr.multiply_ternary(numpy {'float32' if fp32 else 'int32'} v, idx)"
                         + (" on every rank's shard (no collective: each rank's slice returns to its host)"
                            if world > 1 else "")},
@@ -572,10 +574,13 @@ def run_batch(args, cfg, idx, v, ref, kp, kn, k, preprocess_s, world, rank, dist
         "n_gpus": world, "steps": steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": desc, "n": n, "m": m, "k": k, "batch": B,
-                   "form": "per-vector scatter (index L2-resident)" if loop else "batched gather",
+                   "form": "packed-pair scatter: two vectors per reduction, guard-checked (index L2-resident)"
+                           if loop else "batched gather",
                    "l2": "index (97.8 MB) stays L2-resident across the batch: that residency is the amortisation",
                    "preprocess_s": round(preprocess_s, 4)},
-        "gpu_launches": steps * (B if loop else 2),
+        # loop: the guard + one packed-pair scatter launch per two vectors (csrc/capi.cu)
+        # (+ transpose and gather of every vector's short last block when m % k != 0)
+        "gpu_launches": steps * (1 + B // 2 + B % 2 + (2 if m % k else 0) if loop else 2),
         "e2e": {"value": B * 1e3 / e2e_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * B * n,
                 "d2h_bytes_per_step": 4 * B * m, "path": "rsr.multiply_batched(pinned V.cuda(), idx) -> host"},
         "roofline": {"bound": "hbm", "achieved": canonical / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",

@@ -85,13 +85,14 @@ struct BatchParams {
   void* out;
   int64_t rows, cols, row_stride, seg_stride, ld, batch;
   int k, halves;
+  int b_begin;  // first column block of the launch (grid.x covers [b_begin, b_begin + grid.x))
 };
 
 template <typename T, int VW, bool FOLDPP, bool PERM16>
 __global__ void __launch_bounds__(kBatchWarps * 32) batched_kernel(const BatchParams p) {
   using PermT = typename std::conditional<PERM16, uint16_t, uint32_t>::type;
   extern __shared__ __align__(16) unsigned char bsm[];
-  const int b = blockIdx.x, slice = blockIdx.y;
+  const int b = p.b_begin + (int)blockIdx.x, slice = blockIdx.y;
   const int w = block_width(p.cols, p.k, b);
   const int nbk = 1 << w;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(kBatchWarps * 32) batched_kernel(const BatchPa
 
 template <typename T>
 rsr_status launch_batched_t(const rsr_index_desc& d, const void* V, int64_t batch, void* out, bool pp, void* ws,
-                            cudaStream_t s) {
+                            cudaStream_t s, int b0, int b1) {
   const int vw = batch <= 32 ? 1 : batch <= 64 ? 2 : 4;
   const int64_t sw = 32 * vw;                      // vectors per slice
   const int64_t ld = (batch + sw - 1) / sw * sw;   // padded batch
@@ -293,13 +294,14 @@ rsr_status launch_batched_t(const rsr_index_desc& d, const void* V, int64_t batc
   p.batch = batch;
   p.k = d.k;
   p.halves = d.halves;
+  p.b_begin = b0;
   const size_t seg_bytes = (size_t)d.halves * (((size_t)1 << d.k) + 1) * 4;
   const size_t red_bytes = (size_t)kBatchWarps * d.k * sw * sizeof(T);
   const size_t smem = std::max(seg_bytes, red_bytes);
   if (smem > device_max_smem_optin()) return fail(RSR_ERR_UNSUPPORTED, "batched multiply: k too large for shared memory");
   if ((uint64_t)d.rows * (uint64_t)ld >= (1ull << 32))
     return fail(RSR_ERR_UNSUPPORTED, "batched multiply: rows * padded batch must be < 2^32");
-  dim3 grid((unsigned)d.nblocks, (unsigned)(ld / sw));
+  dim3 grid((unsigned)(b1 - b0), (unsigned)(ld / sw));
   auto go = [&](auto kern) -> rsr_status {
     if (smem > 48 * 1024) {
       rsr_status a = set_max_smem((const void*)kern, smem);
@@ -326,17 +328,88 @@ size_t batched_workspace_bytes(const rsr_index_desc& d, int64_t batch, rsr_dtype
   return (size_t)d.rows * (size_t)((batch + sw - 1) / sw * sw) * 4;
 }
 
+// Short last block of an int32 batch (capi.cu packed-pair path): its few key bits make buckets
+// heavy, so it is computed densely.  tail_keys_kernel: key of every row from perm + seg (the
+// bucket holding sorted position p is the largest j with seg[j] <= p, indexer.py:176-186);
+// tail_dense_kernel: grid (vector, row split), out[c] += sum_r v[r] * (bit_c(key+[r]) - bit_c(key-[r]))
+// over the split's rows, int32 reductions (exact modulo 2^32 like every int32 path; out zeroed).
+__global__ void tail_keys_kernel(const rsr_index_desc d, int b, uint16_t* keys) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int h = blockIdx.y;
+  if (p >= d.rows) return;
+  const int w = block_width(d.cols, d.k, b);
+  const uint32_t* seg = (h ? d.half[1].seg : d.half[0].seg) + (int64_t)b * d.seg_stride;
+  int lo = 0, hi = (1 << w) - 1;  // largest j in [0, 2^w) with seg[j] <= p (seg[0] = 0)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((int64_t)__ldg(seg + mid) <= p) lo = mid;
+    else hi = mid - 1;
+  }
+  const int64_t off = (int64_t)b * d.row_stride + p;
+  const void* perm = h ? d.half[1].perm : d.half[0].perm;
+  const int64_t row = d.perm_bytes == 2 ? (int64_t)__ldg(reinterpret_cast<const uint16_t*>(perm) + off)
+                                        : (int64_t)__ldg(reinterpret_cast<const uint32_t*>(perm) + off);
+  keys[h * d.rows + row] = (uint16_t)lo;
+}
+
+__global__ void __launch_bounds__(256) tail_dense_kernel(const rsr_index_desc d, int b, const uint16_t* __restrict__ keys,
+                                                         const int32_t* __restrict__ V, int32_t* __restrict__ out) {
+  const int64_t vec = blockIdx.x;
+  const int w = block_width(d.cols, d.k, b);
+  const int32_t* v = V + vec * d.rows;
+  int32_t acc[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) acc[c] = 0;
+  const int64_t chunk = (d.rows + gridDim.y - 1) / gridDim.y;
+  const int64_t r1 = std::min<int64_t>(d.rows, (blockIdx.y + 1) * chunk);
+  for (int64_t r = blockIdx.y * chunk + threadIdx.x; r < r1; r += blockDim.x) {
+    const int32_t x = __ldg(v + r);
+    const uint32_t kp = __ldg(keys + r);
+    const uint32_t kn = d.halves == 2 ? __ldg(keys + d.rows + r) : 0u;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] += (int32_t)(((kp >> c) & 1u) - ((kn >> c) & 1u)) * x;
+  }
+  __shared__ int32_t part[8][16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const int32_t s = __reduce_add_sync(0xffffffffu, acc[c]);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < w) {  // column c of the block = key bit w - 1 - c (MSB-first)
+    const int bit = w - 1 - threadIdx.x;
+    int32_t s = 0;
+    for (int i = 0; i < 8; ++i) s += part[i][bit];
+    if (s != 0) atomicAdd(out + vec * d.cols + (int64_t)b * d.k + threadIdx.x, s);
+  }
+}
+
+rsr_status multiply_batched_tail(const rsr_index_desc& d, int b, const int32_t* V, int64_t batch, int32_t* out, void* ws,
+                                 cudaStream_t s) {
+  uint16_t* keys = reinterpret_cast<uint16_t*>(ws);
+  tail_keys_kernel<<<dim3((unsigned)((d.rows + 255) / 256), (unsigned)d.halves), 256, 0, s>>>(d, b, keys);
+  rsr_status st = cuda_check(cudaGetLastError(), "tail_keys_kernel launch");
+  if (st != RSR_OK) return st;
+  const int w = block_width(d.cols, d.k, b);
+  st = cuda_check(cudaMemset2DAsync(out + (int64_t)b * d.k, d.cols * 4, 0, w * 4, batch, s), "memset tail");
+  if (st != RSR_OK) return st;
+  const unsigned splits = (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (d.rows + 1023) / 1024));
+  tail_dense_kernel<<<dim3((unsigned)batch, splits), 256, 0, s>>>(d, b, keys, V, out);
+  return cuda_check(cudaGetLastError(), "tail_dense_kernel launch");
+}
+
 rsr_status multiply_batched(const rsr_index_desc& d, const void* V, rsr_dtype vt, int64_t batch, void* out,
-                            rsr_dtype ot, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s) {
-  if (batch == 0) return RSR_OK;
+                            rsr_dtype ot, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s, int b0, int b1) {
+  if (b1 < 0) b1 = d.nblocks;
+  if (batch == 0 || b0 >= b1) return RSR_OK;
   if (vt != ot) return fail(RSR_ERR_INVALID, "batched multiply writes the activation dtype");
   if (vt == RSR_F64) return fail(RSR_ERR_UNSUPPORTED, "batched kernel takes int32 or fp32 activations");
   if (d.k > kMaxW) return fail(RSR_ERR_UNSUPPORTED, "batched multiply supports k <= 16");
   if (!ws || ws_bytes < batched_workspace_bytes(d, batch, vt))
     return fail(RSR_ERR_INVALID, "batched multiply: workspace too small (rsr_multiply_batched_workspace_bytes)");
   const bool pp = var == RSR_VARIANT_RSRPP;
-  if (vt == RSR_I32) return launch_batched_t<int32_t>(d, V, batch, out, pp, ws, s);
-  return launch_batched_t<float>(d, V, batch, out, pp, ws, s);
+  if (vt == RSR_I32) return launch_batched_t<int32_t>(d, V, batch, out, pp, ws, s, b0, b1);
+  return launch_batched_t<float>(d, V, batch, out, pp, ws, s, b0, b1);
 }
 
 }  // namespace rsr

@@ -33,7 +33,10 @@ rsr_status index_import(const rsr_index_desc* d, const uint32_t* perm0, const ui
                         cudaStream_t s);
 
 rsr_status multiply_batched(const rsr_index_desc& d, const void* V, rsr_dtype vt, int64_t batch, void* out,
-                            rsr_dtype ot, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s);
+                            rsr_dtype ot, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s, int b0 = 0,
+                            int b1 = -1);
+rsr_status multiply_batched_tail(const rsr_index_desc& d, int b, const int32_t* V, int64_t batch, int32_t* out, void* ws,
+                                 cudaStream_t s);
 
 namespace {
 thread_local std::string g_last_error;
@@ -210,7 +213,48 @@ rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_d
   }
   if (loop) {  // one multiply per vector
     const size_t vsz = v_dtype == RSR_F64 ? 8 : 4, osz = out_dtype == RSR_F64 ? 8 : 4;
-    for (int64_t i = 0; i < batch; ++i) {
+    int64_t i = 0;
+    // int32 pairs: one scatter launch per two vectors (v + v' * 2^16 in every reduction) when the
+    // guard proves every bucket sum fits in int16; the guard costs one host sync, so not while
+    // the stream is being captured.  RSR_B200_PACK=0 disables it (diagnostics).
+    static const bool env_nopack = getenv("RSR_B200_PACK") && getenv("RSR_B200_PACK")[0] == '0';
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    // Pairs cover the full-width blocks; a short last block (few key bits, so heavy buckets) goes
+    // to the batched gather kernel for all vectors at once.
+    const int nfull = desc->cols % desc->k == 0 ? desc->nblocks : desc->nblocks - 1;
+    if (v_dtype == RSR_I32 && out_dtype == RSR_I32 && batch >= 2 && nfull > 0 && !env_nopack && workspace &&
+        workspace_bytes >= batched_workspace_bytes(*desc, batch, v_dtype) &&
+        (uint64_t)desc->rows * (uint64_t)((batch + 127) / 128 * 128) < (1ull << 32) &&
+        cudaStreamIsCapturing((cudaStream_t)stream, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
+      uint32_t* res = reinterpret_cast<uint32_t*>(workspace);
+      uint32_t h[2] = {0, 0};
+      st = cuda_check(cudaMemsetAsync(res, 0, 8, (cudaStream_t)stream), "memset guard");
+      if (st == RSR_OK) st = rsr::pack_guard(*desc, nfull, (const int32_t*)V, batch * desc->rows, res, (cudaStream_t)stream);
+      if (st == RSR_OK) st = cuda_check(cudaMemcpyAsync(h, res, 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream), "guard copy");
+      if (st == RSR_OK) st = cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "guard sync");
+      if (st != RSR_OK) return st;
+      if ((uint64_t)h[0] * h[1] <= 32767u) {
+        for (; i + 2 <= batch; i += 2) {
+          const int32_t* va = (const int32_t*)V + i * desc->rows;
+          int32_t* oa = (int32_t*)OUT + i * desc->cols;
+          st = rsr::multiply_pair(*desc, nfull, va, va + desc->rows, oa, oa + desc->cols, variant, (cudaStream_t)stream,
+                                  i > 0);
+          if (st != RSR_OK) return st;
+        }
+        if (nfull < desc->nblocks) {  // every vector's short last block (unpaired one included)
+          st = multiply_batched_tail(*desc, nfull, (const int32_t*)V, batch, (int32_t*)OUT, workspace,
+                                     (cudaStream_t)stream);
+          if (st != RSR_OK) return st;
+        }
+        for (; i < batch; ++i) {  // the unpaired vector: its full-width blocks
+          st = multiply(*desc, (const char*)V + i * desc->rows * vsz, v_dtype, (char*)OUT + i * desc->cols * osz,
+                        out_dtype, variant, RSR_FORM_AUTO, 0, nfull, (cudaStream_t)stream, nullptr, nullptr, false);
+          if (st != RSR_OK) return st;
+        }
+        return RSR_OK;
+      }
+    }
+    for (; i < batch; ++i) {
       // vector i > 0 depends only on what vector 0's launch already waited for: its launch
       // overlaps the previous vector's tail (distinct V row and OUT row)
       st = multiply(*desc, (const char*)V + i * desc->rows * vsz, v_dtype, (char*)OUT + i * desc->cols * osz, out_dtype,

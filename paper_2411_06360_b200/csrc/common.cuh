@@ -179,4 +179,13 @@ rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* 
                     rsr_form form, int b0, int b1, cudaStream_t s, const Publish* pub = nullptr,
                     bool* published = nullptr, bool independent = false);
 
+// multiply.cu, batched int32 path: the packed-pair guard and the pair multiply.
+// pack_guard: res[0] = max over blocks [0, b1) and logical bins j >= 1 of the bucket load (rows of key j
+// over both halves), res[1] = max |V| over nv activations (res caller-zeroed, device).
+rsr_status pack_guard(const rsr_index_desc& d, int b1, const int32_t* V, int64_t nv, uint32_t* res, cudaStream_t s);
+// va and vb in one scatter launch (v + vb * 2^16 per reduction): exact iff the guard's
+// load * max|v| <= 32767.  int32 in, int32 out, blocks [0, b1).
+rsr_status multiply_pair(const rsr_index_desc& d, int b1, const int32_t* va, const int32_t* vb, int32_t* outa, int32_t* outb,
+                         rsr_variant var, cudaStream_t s, bool independent);
+
 }  // namespace rsr

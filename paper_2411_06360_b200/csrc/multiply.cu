@@ -104,6 +104,8 @@ struct ScatterParams {
   const uint16_t* key[2];
   const int32_t* v;
   void* out;
+  const int32_t* v2;  // PACK: second vector (bits 16-31 of each packed activation)
+  void* out2;         // PACK: its output
   int64_t rows, cols, row_stride;
   int k, halves, b_begin, b_end;
   int rows_per_cta, n_splits, stages, atomic_out, nhist;
@@ -176,12 +178,19 @@ __device__ __forceinline__ double pow2d(int e) {  // 2^e for |e| <= 1022
 // them fit on an SM (the register budget stays that of the largest CTA: 96 per thread)
 // CODES: 0 = byte-offset codes in row order (k = 14), 1 = scheduled byte-offset codes (k <= 11),
 // 2 = scheduled word-index codes (k = 12, 13; see common.cuh encode_key)
-template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, int CODES, int FW>
+// PACK (int32 vector pairs, batched path): v2 rides in bits 16-31 of every activation, so one
+// reduction serves two vectors.  Exact when every bucket sum of either vector fits in int16
+// (the host guard: max bucket load x max |v| <= 32767, bin 0 excluded — the fold never adds
+// logical bin 0 into an output); the fold warps split each bin into its two int16 halves,
+// fold both, and zero the buffer after reading (a per-block value per bin, no running total).
+template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, int CODES, int FW, bool PACK = false>
 __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
   static_assert(FW == 1 || FW == 2 || FW == 4 || FW == 8, "fold warps");
+  static_assert(!(PACK && FX) && (!PACK || std::is_same<OutT, int32_t>::value), "PACK: int32 only");
   constexpr int FB = FW == 8 ? 3 : FW == 4 ? 2 : FW == 2 ? 1 : 0;  // key bits spanned by the fold warps
   static_assert(R % 8 == 0 && R * kScatterThreads <= 32768, "rows per CTA");
-  constexpr int LIMBS = FX ? 2 : 1;
+  constexpr int LIMBS = FX ? 2 : 1;              // histogram limbs
+  constexpr int OLIMBS = (FX || PACK) ? 2 : 1;   // fold results per slot
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int HALVES = TERNARY ? 2 : 1;
   constexpr int NG = R / 8;      // 8-row groups per lane
@@ -209,6 +218,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   const uint16_t* key0 = p.key[0];
   const uint16_t* key1 = p.key[1];
   OutT* out = reinterpret_cast<OutT*>(p.out);
+  OutT* out2 = reinterpret_cast<OutT*>(p.out2);
   const bool is_fold = warp >= nwarps;
   if (warp == 0) TRACE(0);
 
@@ -236,7 +246,10 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     for (int i = t; i < nunits * p.k; i += blockDim.x) {
       const int b = p.b_begin + col_cta + (i / p.k) * ncol;
       const int c = i % p.k;
-      if (c < block_width(p.cols, p.k, b)) out[(int64_t)b * p.k + c] = (OutT)0;
+      if (c < block_width(p.cols, p.k, b)) {
+        out[(int64_t)b * p.k + c] = (OutT)0;
+        if constexpr (PACK) out2[(int64_t)b * p.k + c] = (OutT)0;
+      }
     }
 
   if (!is_fold) {
@@ -282,6 +295,24 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       } else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;  // rows past the end: 0
+      }
+    }
+    if constexpr (PACK) {  // packed = v + v2 * 2^16 (mod 2^32)
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const int64_t row = wr0 + 256 * g + 8 * lane;
+        const int32_t* vp = p.v2 + row;
+        int32_t b[8];
+        if (row + 8 <= p.rows && p.v_aligned) {
+          const int4 a = __ldg(reinterpret_cast<const int4*>(vp));
+          const int4 c = __ldg(reinterpret_cast<const int4*>(vp) + 1);
+          b[0] = a.x; b[1] = a.y; b[2] = a.z; b[3] = a.w; b[4] = c.x; b[5] = c.y; b[6] = c.z; b[7] = c.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) b[e] = (row + e < p.rows) ? vp[e] : 0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) vr[8 * g + e] = (int32_t)((uint32_t)vr[8 * g + e] + ((uint32_t)b[e] << 16));
       }
     }
     if constexpr (FX) {  // CTA max |v| -> quantization scale
@@ -394,9 +425,9 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     if (lb < 0) lb = 0;
     const int fbase = (fw * 32 + lane) << lb;
     const bool active = fbase < nbk;
-    int32_t prev[LIMBS][MAXNH];
+    int32_t prev[OLIMBS][MAXNH];
 #pragma unroll
-    for (int l = 0; l < LIMBS; ++l)
+    for (int l = 0; l < OLIMBS; ++l)
 #pragma unroll
       for (int i = 0; i < MAXNH; ++i) prev[l][i] = 0;
     int fx_e = 0;
@@ -407,7 +438,14 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     else if (lane < 13) sh = lb + (lane - 8);
     else if (lane < 13 + FB) sh = lb + 5 + (lane - 13);
     // per-lane partials of my bins of one limb histogram, then REDUX over the warp: lane i -> slot i
-    auto fold_limb = [&](const int32_t* H) -> int32_t {
+    // SEL: 0 the bin as stored, 1 / 2 the low / high int16 half of a packed bin
+    auto fold_limb = [&](const int32_t* H, auto selc) -> int32_t {
+      constexpr int SEL = decltype(selc)::value;
+      auto unpack = [](int32_t x) -> int32_t {
+        if constexpr (SEL == 1) return (int32_t)(int16_t)x;
+        else if constexpr (SEL == 2) return (int32_t)((uint32_t)x - (uint32_t)(int32_t)(int16_t)x) >> 16;
+        else return x;
+      };
       int32_t a[8];  // local-bit partials, lb <= 7
 #pragma unroll
       for (int i = 0; i < 8; ++i) a[i] = 0;
@@ -426,6 +464,8 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
             }
             int32_t x[16] = {z[0].x, z[0].y, z[0].z, z[0].w, z[1].x, z[1].y, z[1].z, z[1].w,
                              z[2].x, z[2].y, z[2].z, z[2].w, z[3].x, z[3].y, z[3].z, z[3].w};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = unpack(x[i]);
             int32_t tot = 0;
             if (FOLDPP) {  // pairwise compaction over the 4 bits inside the 16-bin chunk
 #pragma unroll
@@ -459,7 +499,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (e < (1 << lb)) {
-              const int32_t x = H[key_swizzle((uint32_t)(fbase + e))];
+              const int32_t x = unpack(H[key_swizzle((uint32_t)(fbase + e))]);
               if (lb >= 1 && (e & 1)) a[0] += x;
               X += x;
             }
@@ -490,15 +530,31 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       if (fw == 0 && f < 40) TRACE(8 + f * 8 + 3);
       mbar_wait(&hfull[fb], fpar);
       if (fw == 0 && f < 40) TRACE(8 + f * 8 + 4);
-      int32_t d[LIMBS];  // this block's slot value per limb: fold(H now) - fold(H after block f - NH)
+      int32_t d[OLIMBS];  // this block's slot value per limb: fold(H now) - fold(H after block f - NH)
+      if constexpr (PACK) {
+        d[0] = fold_limb(H, std::integral_constant<int, 1>{});
+        d[1] = fold_limb(H, std::integral_constant<int, 2>{});
+        if (active) {  // zero my bins: the next block in this buffer starts from 0
+          int32_t* Hw = const_cast<int32_t*>(H);
+          if (lb >= 2) {
+            for (int c4 = 0; c4 < (1 << (lb - 2)); ++c4) {
+              const int j4 = (fbase >> 2) + c4;
+              reinterpret_cast<int4*>(Hw)[j4 ^ (int)((((uint32_t)j4 >> 3) & 31u) >> 2)] = make_int4(0, 0, 0, 0);
+            }
+          } else {
+            for (int e = 0; e < (1 << lb); ++e) Hw[key_swizzle((uint32_t)(fbase + e))] = 0;
+          }
+        }
+      } else {
 #pragma unroll
-      for (int l = 0; l < LIMBS; ++l) {
-        const int32_t r = fold_limb(H + l * nbk);
-        int32_t pv = 0;
+        for (int l = 0; l < LIMBS; ++l) {
+          const int32_t r = fold_limb(H + l * nbk, std::integral_constant<int, 0>{});
+          int32_t pv = 0;
 #pragma unroll
-        for (int i = 0; i < MAXNH; ++i)
-          if (i == fb) { pv = prev[l][i]; prev[l][i] = r; }
-        d[l] = r - pv;
+          for (int i = 0; i < MAXNH; ++i)
+            if (i == fb) { pv = prev[l][i]; prev[l][i] = r; }
+          d[l] = r - pv;
+        }
       }
       __syncwarp();
       if (fw == 0 && f < 40) TRACE(8 + f * 8 + 5);
@@ -518,6 +574,8 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         }
       } else {
         if (sh >= 0 && sh < w && d[0] != 0) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)d[0]);
+        if constexpr (PACK)
+          if (sh >= 0 && sh < w && d[OLIMBS - 1] != 0) atomicAdd(out2 + (int64_t)b * p.k + (w - 1 - sh), (OutT)d[OLIMBS - 1]);
       }
       if (fw == 0 && f < 40) TRACE(400 + f);
     }
@@ -872,13 +930,13 @@ static bool pdl_enabled() {
   return on == 1;
 }
 
-template <bool PP, typename OutT, bool FX, int FW>
+template <bool PP, typename OutT, bool FX, int FW, bool PACK>
 rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int threads, cudaStream_t s) {
   auto pick = [&](auto ternary) {
     constexpr bool T = decltype(ternary)::value;
-    return p.codes == 1 ? scatter_kernel<kScatterR, PP, T, OutT, FX, 1, FW>
-           : p.codes == 2 ? scatter_kernel<kScatterR, PP, T, OutT, FX, 2, FW>
-                          : scatter_kernel<kScatterR, PP, T, OutT, FX, 0, FW>;
+    return p.codes == 1 ? scatter_kernel<kScatterR, PP, T, OutT, FX, 1, FW, PACK>
+           : p.codes == 2 ? scatter_kernel<kScatterR, PP, T, OutT, FX, 2, FW, PACK>
+                          : scatter_kernel<kScatterR, PP, T, OutT, FX, 0, FW, PACK>;
   };
   auto kern = p.halves == 2 ? pick(std::true_type{}) : pick(std::false_type{});
   rsr_status st = set_max_smem((const void*)kern, smem);
@@ -896,21 +954,27 @@ rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int t
   return cuda_check(cudaLaunchKernelEx(&cfg, kern, p), "scatter_kernel launch");
 }
 
-template <bool PP, typename OutT, bool FX>
+template <bool PP, typename OutT, bool FX, bool PACK = false>
 rsr_status launch_scatter_fw(const ScatterParams& p, int grid, size_t smem, int threads, int fw, cudaStream_t s) {
-  return fw == 1 ? launch_scatter_t<PP, OutT, FX, 1>(p, grid, smem, threads, s)
-                 : launch_scatter_t<PP, OutT, FX, kFoldWarps>(p, grid, smem, threads, s);
+  return fw == 1 ? launch_scatter_t<PP, OutT, FX, 1, PACK>(p, grid, smem, threads, s)
+                 : launch_scatter_t<PP, OutT, FX, kFoldWarps, PACK>(p, grid, smem, threads, s);
 }
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, void* out, rsr_dtype out_dtype, bool pp,
-                            int b0, int b1, cudaStream_t s, const Publish* pub, bool* published, bool independent) {
+                            int b0, int b1, cudaStream_t s, const Publish* pub, bool* published, bool independent,
+                            const void* v2 = nullptr, void* out2 = nullptr) {
   if (d.k > 14) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply supports k <= 14");
+  const bool pack = v2 != nullptr;
+  if (pack && (fx || out_dtype != RSR_I32 || pub))
+    return fail(RSR_ERR_INVALID, "packed pair multiply: int32 activations and output only");
   ScatterParams p{};
+  p.v2 = reinterpret_cast<const int32_t*>(v2);
+  p.out2 = out2;
   p.independent = independent ? 1 : 0;
   const bool publish = pub && out_dtype != RSR_F64;  // single split only (decided below)
   for (int h = 0; h < d.halves; ++h) p.key[h] = d.half[h].bucket;
   p.v = reinterpret_cast<const int32_t*>(v);
-  p.v_aligned = ((uintptr_t)v & 15) == 0;
+  p.v_aligned = ((uintptr_t)v & 15) == 0 && ((uintptr_t)v2 & 15) == 0;
   p.out = out;
   p.rows = d.rows;
   p.cols = d.cols;
@@ -972,7 +1036,14 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
     const int64_t c1 = std::min<int64_t>(d.cols, (int64_t)b1 * d.k);
     rsr_status st = cuda_check(cudaMemsetAsync((char*)out + c0 * esz, 0, (c1 - c0) * esz, s), "memset out");
     if (st != RSR_OK) return st;
+    if (pack) {
+      st = cuda_check(cudaMemsetAsync((char*)out2 + c0 * esz, 0, (c1 - c0) * esz, s), "memset out2");
+      if (st != RSR_OK) return st;
+    }
   }
+  if (pack)
+    return pp ? launch_scatter_fw<true, int32_t, false, true>(p, grid, smem, threads, fw, s)
+              : launch_scatter_fw<false, int32_t, false, true>(p, grid, smem, threads, fw, s);
   if (fx)
     return pp ? launch_scatter_fw<true, float, true>(p, grid, smem, threads, fw, s)
               : launch_scatter_fw<false, float, true>(p, grid, smem, threads, fw, s);
@@ -1052,6 +1123,64 @@ rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* 
     case RSR_F64: return multiply_gather_t<double>(d, v, out, pp, b0, b1, s);
   }
   return fail(RSR_ERR_INVALID, "unknown dtype");
+}
+
+namespace {
+// grid-stride over (block, bin) pairs, then over the activations; warp max, one atomic per warp
+// grid (bins / 256, ceil(b1 / 4) + 128): rows below ceil(b1 / 4) cover 4 blocks' bins each
+// (coalesced seg reads), the last 128 rows the activations (grid-stride); CTA max, then one
+// atomic per CTA (same-address atomics from every warp serialise at L2)
+__global__ void __launch_bounds__(256) pack_guard_kernel(const rsr_index_desc d, int b1, const int32_t* __restrict__ V,
+                                                         int64_t nv, uint32_t* res) {
+  constexpr int kBlocksPerRow = 4, kVRows = 128;
+  uint32_t m = 0;
+  const int brows = (b1 + kBlocksPerRow - 1) / kBlocksPerRow;
+  const bool is_bins = (int)blockIdx.y < brows;
+  if (is_bins) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < kBlocksPerRow; ++q) {
+      const int b = blockIdx.y * kBlocksPerRow + q;
+      if (b < b1 && j >= 1 && j < ((int64_t)1 << block_width(d.cols, d.k, b))) {
+        uint32_t load = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)  // constant half index: the descriptor stays in param space
+          if (h < d.halves) {
+            const uint32_t* seg = d.half[h].seg + (int64_t)b * d.seg_stride;
+            load += __ldg(seg + j + 1) - __ldg(seg + j);
+          }
+        m = max(m, load);
+      }
+    }
+  } else {
+    const int64_t stride = (int64_t)kVRows * gridDim.x * blockDim.x;
+    for (int64_t i = ((int64_t)(blockIdx.y - brows) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; i < nv;
+         i += stride) {
+      const int32_t x = V[i];
+      m = max(m, x < 0 ? 0u - (uint32_t)x : (uint32_t)x);
+    }
+  }
+  __shared__ uint32_t wm[8];
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, wm[i]);
+    if (m) atomicMax(res + (is_bins ? 0 : 1), m);
+  }
+}
+}  // namespace
+
+rsr_status pack_guard(const rsr_index_desc& d, int b1, const int32_t* V, int64_t nv, uint32_t* res, cudaStream_t s) {
+  const dim3 grid((unsigned)std::max<int64_t>(8, (((int64_t)1 << d.k) + 255) / 256), (unsigned)((b1 + 3) / 4 + 128));
+  pack_guard_kernel<<<grid, 256, 0, s>>>(d, b1, V, nv, res);
+  return cuda_check(cudaGetLastError(), "pack_guard_kernel launch");
+}
+
+rsr_status multiply_pair(const rsr_index_desc& d, int b1, const int32_t* va, const int32_t* vb, int32_t* outa,
+                         int32_t* outb, rsr_variant var, cudaStream_t s, bool independent) {
+  return multiply_scatter(d, va, false, outa, RSR_I32, var == RSR_VARIANT_RSRPP, 0, b1, s, nullptr, nullptr,
+                          independent, vb, outb);
 }
 
 rsr_status segmented_sum(const rsr_index_desc& d, int half, int block, const void* v, rsr_dtype dt, void* u,

@@ -486,3 +486,39 @@ def test_host_session_threads_and_errors(rsr, cuda):
     assert not errors
     with pytest.raises(ValueError, match="does not match"):
         rsr.multiply_ternary(vs[0][:100], idx)
+
+
+@pytest.mark.parametrize("rows,cols,k,batch,vmax", [
+    (64, 5, 5, 2, 511),        # one full bin: 64 * 511 = 32704, at the int16 edge (packed)
+    (64, 5, 5, 3, 512),        # 64 * 512 = 32768: the guard refuses, per-vector path
+    (1003, 37, 6, 5, 100),     # ragged rows / last block, odd batch (one unpaired vector)
+    (16384, 600, 11, 8, 100),  # the headline block width, full CTAs
+    (4096, 333, 10, 6, 2**31 - 1),
+])
+def test_batched_packed_pairs(rsr, cuda, rows, cols, k, batch, vmax):
+    """The int32 batched loop runs two vectors per scatter launch (v + v' * 2^16 per
+    reduction) when max bucket load * max |v| <= 32767 (csrc/capi.cu, multiply.cu PACK):
+    results must equal the reference per vector on both sides of that guard."""
+    import torch
+    rng = np.random.default_rng([rows, cols, k, batch, vmax])
+    if rows == 64:
+        A = np.ones((rows, cols), dtype=np.int8)  # every row in logical bin 2^k - 1
+        Vi = np.full((batch, rows), vmax, dtype=np.int32)
+        Vi[1::2] = -vmax
+    else:
+        A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+        Vi = rng.integers(-vmax, vmax, size=(batch, rows), endpoint=True, dtype=np.int64).astype(np.int32)
+    tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+    for variant in ("rsrpp", "rsr"):
+        got = rsr.multiply_batched(torch.from_numpy(Vi).cuda(), tidx, variant).cpu().numpy()
+        for i in range(batch):
+            one = rsr.multiply_ternary(torch.from_numpy(Vi[i].copy()).cuda(), tidx, variant).cpu().numpy()
+            assert np.array_equal(got[i], one), (variant, i)
+        if vmax <= 512:
+            ref = (Vi.astype(np.int64) @ A.astype(np.int64))
+            assert np.array_equal(got.astype(np.int64), ref), variant
+    B = (A == 1).astype(np.uint8)
+    bidx = rsr.preprocess(rsr.BinaryMatrix.from_dense(B), k)
+    gotb = rsr.multiply_batched(torch.from_numpy(Vi).cuda(), bidx).cpu().numpy()
+    refb = (Vi.astype(np.int64) @ B.astype(np.int64))
+    assert np.array_equal(gotb.astype(np.int64), (refb + 2**31) % 2**32 - 2**31)
