@@ -143,13 +143,16 @@ rsr_status rsr_dense_pack_ternary(const int8_t* A, int64_t lda, int64_t rows, in
 rsr_status rsr_dense_multiply(const uint32_t* d_pos, const uint32_t* d_neg, int64_t rows, int64_t cols,
                               const void* v, rsr_dtype dtype, void* out, void* stream);
 
-/* Batched multiply: V [batch][rows] -> OUT [batch][cols] on the current stream, every index
- * byte read once per slice of up to 128 vectors instead of once per vector (SURVEY.md §8(d)
- * config 3; the reference has no batch API and runs `multiply_ternary`, kernels.py:196-206,
- * once per vector).  int32 (exact) and fp32 activations run the batched gather kernel and
- * need `workspace` of rsr_multiply_batched_workspace_bytes() bytes (device, 16-byte aligned;
- * holds V transposed); out_dtype must equal v_dtype.  fp64 runs one multiply per vector
- * (workspace unused). */
+/* Batched multiply: V [batch][rows] -> OUT [batch][cols] on the current stream (SURVEY.md
+ * §8(d) config 3; the reference has no batch API and runs `multiply_ternary`,
+ * kernels.py:196-206, once per vector).  int32 and fp32 need `workspace` of
+ * rsr_multiply_batched_workspace_bytes() bytes (device, 16-byte aligned); out_dtype must equal
+ * v_dtype.  Forms: index beyond L2 -> the batched gather kernel (each index byte read once per
+ * slice of up to 128 vectors, V transposed into the workspace); index L2-resident -> scatter
+ * launches, for int32 two vectors per launch (v + v' * 2^16 per reduction) when a device guard
+ * proves every bucket sum fits in int16 — that guard is ONE host synchronisation of `stream`
+ * per call, skipped (per-vector launches) while the stream is being captured.  Results are
+ * exact for int32 in every form.  fp64 runs one multiply per vector (workspace unused). */
 size_t rsr_multiply_batched_workspace_bytes(const rsr_index_desc* desc, int64_t batch, rsr_dtype v_dtype);
 rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_dtype v_dtype,
                                 int64_t batch, void* OUT, rsr_dtype out_dtype,

@@ -523,6 +523,105 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         if (lane == 13 + fb2) r = ((fw >> fb2) & 1) ? W : 0;
       return r;
     };
+#ifdef RSR_PACK1
+    // PACK, one pass: each packed bin becomes (hi << 32) + lo in 64 bits, so one 64-bit add
+    // accumulates both vectors (|partial sums| < 2^31: no carry crosses into the wrong half
+    // beyond the borrow that the split below undoes)
+    auto fold_pair = [&](const int32_t* H, int32_t& rlo, int32_t& rhi) {
+      auto unpack = [](int32_t x) -> long long {
+        const int32_t lo = (int16_t)x;
+        const int32_t hi = (int32_t)((uint32_t)x - (uint32_t)lo) >> 16;
+        return ((long long)hi << 32) + lo;
+      };
+      long long a[8];  // local-bit partials, lb <= 7
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = 0;
+      long long X = 0;
+      if (active) {
+        const int4* H4 = reinterpret_cast<const int4*>(H);
+        if (lb >= 2) {
+          const int n4 = 1 << (lb - 2);
+          for (int c4 = 0; c4 < n4; c4 += 4) {  // 4 int4 (16 bins) at a time
+            int4 z[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int j4 = (fbase >> 2) + c4 + i;  // logical int4 index
+              const uint32_t c = ((uint32_t)j4 >> 3) & 31u;
+              z[i] = (c4 + i < n4) ? unswizzle4(H4[j4 ^ (int)(c >> 2)], c) : make_int4(0, 0, 0, 0);
+            }
+            long long x[16] = {z[0].x, z[0].y, z[0].z, z[0].w, z[1].x, z[1].y, z[1].z, z[1].w,
+                             z[2].x, z[2].y, z[2].z, z[2].w, z[3].x, z[3].y, z[3].z, z[3].w};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = unpack(x[i]);
+            long long tot = 0;
+            if (FOLDPP) {  // pairwise compaction over the 4 bits inside the 16-bin chunk
+#pragma unroll
+              for (int L = 0; L < 4; ++L) {
+                const int cnt = 8 >> L;
+                long long odd = 0;
+#pragma unroll
+                for (int tt = 0; tt < 8; ++tt)
+                  if (tt < cnt) {
+                    odd += x[2 * tt + 1];
+                    x[tt] = x[2 * tt] + x[2 * tt + 1];
+                  }
+                a[L] += odd;
+              }
+              tot = x[0];
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+#pragma unroll
+                for (int L = 0; L < 4; ++L) a[L] += ((e >> L) & 1) ? x[e] : 0;
+                tot += x[e];
+              }
+            }
+            // chunk bits 4.. (chunk index c4/4) are local bits too
+            const int ci = c4 >> 2;
+#pragma unroll
+            for (int L = 4; L < 8; ++L) a[L] += ((ci >> (L - 4)) & 1) ? tot : 0;
+            X += tot;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e < (1 << lb)) {
+              const long long x = unpack(H[key_swizzle((uint32_t)(fbase + e))]);
+              if (lb >= 1 && (e & 1)) a[0] += x;
+              X += x;
+            }
+        }
+      }
+      auto split = [](long long v, int32_t& lo, int32_t& hi) {
+        lo = (int32_t)v;
+        hi = (int32_t)((v - (long long)lo) >> 32);
+      };
+      rlo = 0; rhi = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < lb) {
+          int32_t l, h;
+          split(a[i], l, h);
+          const int32_t tl = __reduce_add_sync(0xffffffffu, l), th = __reduce_add_sync(0xffffffffu, h);
+          if (lane == i) { rlo = tl; rhi = th; }
+        }
+      int32_t Xl, Xh;
+      split(X, Xl, Xh);
+#pragma unroll
+      for (int bit = 0; bit < 5; ++bit) {
+        const bool on = (lane >> bit) & 1;
+        const int32_t tl = __reduce_add_sync(0xffffffffu, on ? Xl : 0), th = __reduce_add_sync(0xffffffffu, on ? Xh : 0);
+        if (lane == 8 + bit) { rlo = tl; rhi = th; }
+      }
+      const int32_t Wl = __reduce_add_sync(0xffffffffu, Xl), Wh = __reduce_add_sync(0xffffffffu, Xh);
+#pragma unroll
+      for (int fb2 = 0; fb2 < FB; ++fb2)
+        if (lane == 13 + fb2) {
+          rlo = ((fw >> fb2) & 1) ? Wl : 0;
+          rhi = ((fw >> fb2) & 1) ? Wh : 0;
+        }
+    };
+#endif
     int fb = 0;          // f % NH, kept incrementally
     uint32_t fpar = 0;   // (f / NH) & 1
     for (int f = 0; f < nunits; ++f, (++fb == NH ? (fb = 0, fpar ^= 1u) : 0u)) {
@@ -532,8 +631,12 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       if (fw == 0 && f < 40) TRACE(8 + f * 8 + 4);
       int32_t d[OLIMBS];  // this block's slot value per limb: fold(H now) - fold(H after block f - NH)
       if constexpr (PACK) {
+#ifdef RSR_PACK1
+        fold_pair(H, d[0], d[OLIMBS - 1]);
+#else
         d[0] = fold_limb(H, std::integral_constant<int, 1>{});
         d[1] = fold_limb(H, std::integral_constant<int, 2>{});
+#endif
         if (active) {  // zero my bins: the next block in this buffer starts from 0
           int32_t* Hw = const_cast<int32_t*>(H);
           if (lb >= 2) {

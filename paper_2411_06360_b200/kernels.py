@@ -349,9 +349,11 @@ def multiply_parallel(v, idx, variant: str = "rsrpp", worker_count: int = 1, *, 
 
 
 def multiply_batched(V, idx, variant: str = "rsrpp"):
-    """V [batch, rows] CUDA tensor -> [batch, cols] of the same dtype.  int32 / fp32 run the
+    """V [batch, rows] CUDA tensor -> [batch, cols] of the same dtype.  Index beyond L2: the
     batched gather kernel (csrc/batched.cu: each index byte read once per slice of up to 128
-    vectors); fp64 runs one multiply per vector.  The reference has no batch API: this equals
+    vectors).  Index L2-resident: scatter launches, int32 two vectors per launch when the
+    device guard proves the packing exact (one host sync per call; include/rsr_b200.h).  fp64
+    runs one multiply per vector.  The reference has no batch API: this equals
     `multiply_ternary` / `multiply_rsr` applied to every row of V (kernels.py:185-206)."""
     import torch
     use_fold = _use_fold(variant)
