@@ -522,3 +522,26 @@ def test_batched_packed_pairs(rsr, cuda, rows, cols, k, batch, vmax):
     gotb = rsr.multiply_batched(torch.from_numpy(Vi).cuda(), bidx).cpu().numpy()
     refb = (Vi.astype(np.int64) @ B.astype(np.int64))
     assert np.array_equal(gotb.astype(np.int64), (refb + 2**31) % 2**32 - 2**31)
+
+
+def test_batched_under_graph_capture(rsr, cuda):
+    """Inside CUDA graph capture the int32 batched call must not synchronise (the packed-pair
+    guard needs a host read): it falls back to per-vector launches, with the same results."""
+    import torch
+    rng = np.random.default_rng(7)
+    A = rng.integers(-1, 2, size=(2048, 300), dtype=np.int8)
+    tidx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), 10)
+    V = torch.from_numpy(rng.integers(-100, 101, size=(6, 2048)).astype(np.int32)).cuda()
+    eager = rsr.multiply_batched(V, tidx)  # packed pairs (guard passes), also warms the workspace
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+        captured = rsr.multiply_batched(V, tidx)
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(captured, eager)
+    ref = V.cpu().numpy().astype(np.int64) @ A.astype(np.int64)
+    assert np.array_equal(eager.cpu().numpy().astype(np.int64), ref)
