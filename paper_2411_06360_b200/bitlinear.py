@@ -3,7 +3,9 @@
 A fixed ternary weight matrix W [in_features, out_features] (the reference's v · A
 orientation: activations are row vectors) is preprocessed once into a device index; every
 forward is one `multiply_ternary` (or `multiply_batched` for [B, in] inputs) on the current
-stream — no host syncs, so a chain of layers can be captured in one CUDA graph.  An optional
+stream, and a chain of layers can be captured in one CUDA graph (single vectors never sync;
+an eager int32 [B, in] call syncs once for the packed-pair guard, and under capture it runs
+one launch per vector instead, include/rsr_b200.h).  An optional
 per-output scale (BitNet's absmean weight scale) is applied after the integer/fixed-point
 product.
 """
