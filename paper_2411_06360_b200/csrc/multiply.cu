@@ -182,7 +182,7 @@ __device__ __forceinline__ double pow2d(int e) {  // 2^e for |e| <= 1022
 // reduction serves two vectors.  Exact when every bucket sum of either vector fits in int16
 // (the host guard: max bucket load x max |v| <= 32767, bin 0 excluded — the fold never adds
 // logical bin 0 into an output); the fold warps split each bin into its two int16 halves,
-// fold both in one pass as (hi << 32) + lo in 64-bit adds, and zero the buffer after reading
+// fold both in one int32 pass (the packed words and their high halves), and zero the buffer after reading
 // (a per-block value per bin, no running total).
 template <int R, bool FOLDPP, bool TERNARY, typename OutT, bool FX, int CODES, int FW, bool PACK = false>
 __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_kernel(const ScatterParams p) {
@@ -515,19 +515,16 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         if (lane == 13 + fb2) r = ((fw >> fb2) & 1) ? W : 0;
       return r;
     };
-    // PACK, one pass: each packed bin becomes (hi << 32) + lo in 64 bits, so one 64-bit add
-    // accumulates both vectors (|partial sums| < 2^31: no carry crosses into the wrong half
-    // beyond the borrow that the split below undoes)
+    // PACK, one pass, int32 only: fold the packed words x themselves (wrapping: the sums are
+    // lo + 2^16 hi modulo 2^32) and the high halves hi = (x - (int16)x) >> 16 (exact: every
+    // partial sum is below 2^31 in magnitude); then lo = fold(x) - 2^16 fold(hi) modulo 2^32,
+    // exact for the same reason.  Half the ALU of 64-bit (hi << 32) + lo accumulation.
     auto fold_pair = [&](const int32_t* H, int32_t& rlo, int32_t& rhi) {
-      auto unpack = [](int32_t x) -> long long {
-        const int32_t lo = (int16_t)x;
-        const int32_t hi = (int32_t)((uint32_t)x - (uint32_t)lo) >> 16;
-        return ((long long)hi << 32) + lo;
-      };
-      long long a[8];  // local-bit partials, lb <= 7
+      auto hi16 = [](int32_t x) -> int32_t { return (int32_t)((uint32_t)x - (uint32_t)(int32_t)(int16_t)x) >> 16; };
+      int32_t a[8], b[8];  // local-bit partials of x and hi, lb <= 7
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = 0;
-      long long X = 0;
+      for (int i = 0; i < 8; ++i) a[i] = b[i] = 0;
+      int32_t X = 0, Y = 0;
       if (active) {
         const int4* H4 = reinterpret_cast<const int4*>(H);
         if (lb >= 2) {
@@ -540,76 +537,86 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
               const uint32_t c = ((uint32_t)j4 >> 3) & 31u;
               z[i] = (c4 + i < n4) ? unswizzle4(H4[j4 ^ (int)(c >> 2)], c) : make_int4(0, 0, 0, 0);
             }
-            long long x[16] = {z[0].x, z[0].y, z[0].z, z[0].w, z[1].x, z[1].y, z[1].z, z[1].w,
+            int32_t x[16] = {z[0].x, z[0].y, z[0].z, z[0].w, z[1].x, z[1].y, z[1].z, z[1].w,
                              z[2].x, z[2].y, z[2].z, z[2].w, z[3].x, z[3].y, z[3].z, z[3].w};
+            int32_t y[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = unpack(x[i]);
-            long long tot = 0;
+            for (int i = 0; i < 16; ++i) y[i] = hi16(x[i]);
+            int32_t tot = 0, toty = 0;
             if (FOLDPP) {  // pairwise compaction over the 4 bits inside the 16-bin chunk
 #pragma unroll
               for (int L = 0; L < 4; ++L) {
                 const int cnt = 8 >> L;
-                long long odd = 0;
+                int32_t odd = 0, oddy = 0;
 #pragma unroll
                 for (int tt = 0; tt < 8; ++tt)
                   if (tt < cnt) {
                     odd += x[2 * tt + 1];
+                    oddy += y[2 * tt + 1];
                     x[tt] = x[2 * tt] + x[2 * tt + 1];
+                    y[tt] = y[2 * tt] + y[2 * tt + 1];
                   }
                 a[L] += odd;
+                b[L] += oddy;
               }
               tot = x[0];
+              toty = y[0];
             } else {
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
 #pragma unroll
-                for (int L = 0; L < 4; ++L) a[L] += ((e >> L) & 1) ? x[e] : 0;
+                for (int L = 0; L < 4; ++L) {
+                  a[L] += ((e >> L) & 1) ? x[e] : 0;
+                  b[L] += ((e >> L) & 1) ? y[e] : 0;
+                }
                 tot += x[e];
+                toty += y[e];
               }
             }
-            // chunk bits 4.. (chunk index c4/4) are local bits too
-            const int ci = c4 >> 2;
+            const int ci = c4 >> 2;  // chunk bits 4.. are local bits too
 #pragma unroll
-            for (int L = 4; L < 8; ++L) a[L] += ((ci >> (L - 4)) & 1) ? tot : 0;
+            for (int L = 4; L < 8; ++L) {
+              a[L] += ((ci >> (L - 4)) & 1) ? tot : 0;
+              b[L] += ((ci >> (L - 4)) & 1) ? toty : 0;
+            }
             X += tot;
+            Y += toty;
           }
         } else {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (e < (1 << lb)) {
-              const long long x = unpack(H[key_swizzle((uint32_t)(fbase + e))]);
-              if (lb >= 1 && (e & 1)) a[0] += x;
+              const int32_t x = H[key_swizzle((uint32_t)(fbase + e))];
+              const int32_t y = hi16(x);
+              if (lb >= 1 && (e & 1)) { a[0] += x; b[0] += y; }
               X += x;
+              Y += y;
             }
         }
       }
-      auto split = [](long long v, int32_t& lo, int32_t& hi) {
-        lo = (int32_t)v;
-        hi = (int32_t)((v - (long long)lo) >> 32);
+      auto set = [&](int32_t tx, int32_t ty) {  // slot value of both vectors from fold(x), fold(hi)
+        rhi = ty;
+        rlo = (int32_t)((uint32_t)tx - ((uint32_t)ty << 16));
       };
       rlo = 0; rhi = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         if (i < lb) {
-          int32_t l, h;
-          split(a[i], l, h);
-          const int32_t tl = __reduce_add_sync(0xffffffffu, l), th = __reduce_add_sync(0xffffffffu, h);
-          if (lane == i) { rlo = tl; rhi = th; }
+          const int32_t tx = __reduce_add_sync(0xffffffffu, a[i]), ty = __reduce_add_sync(0xffffffffu, b[i]);
+          if (lane == i) set(tx, ty);
         }
-      int32_t Xl, Xh;
-      split(X, Xl, Xh);
 #pragma unroll
       for (int bit = 0; bit < 5; ++bit) {
         const bool on = (lane >> bit) & 1;
-        const int32_t tl = __reduce_add_sync(0xffffffffu, on ? Xl : 0), th = __reduce_add_sync(0xffffffffu, on ? Xh : 0);
-        if (lane == 8 + bit) { rlo = tl; rhi = th; }
+        const int32_t tx = __reduce_add_sync(0xffffffffu, on ? X : 0), ty = __reduce_add_sync(0xffffffffu, on ? Y : 0);
+        if (lane == 8 + bit) set(tx, ty);
       }
-      const int32_t Wl = __reduce_add_sync(0xffffffffu, Xl), Wh = __reduce_add_sync(0xffffffffu, Xh);
+      const int32_t Wx = __reduce_add_sync(0xffffffffu, X), Wy = __reduce_add_sync(0xffffffffu, Y);
 #pragma unroll
       for (int fb2 = 0; fb2 < FB; ++fb2)
         if (lane == 13 + fb2) {
-          rlo = ((fw >> fb2) & 1) ? Wl : 0;
-          rhi = ((fw >> fb2) & 1) ? Wh : 0;
+          if ((fw >> fb2) & 1) set(Wx, Wy);
+          else set(0, 0);
         }
     };
     int fb = 0;          // f % NH, kept incrementally
