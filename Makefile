@@ -3,10 +3,14 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 SRC := $(wildcard paper_2411_06360_b200/csrc/*.cu)
-HDR := $(wildcard paper_2411_06360_b200/csrc/*.cuh) include/rsr_b200.h
+HDR := $(wildcard paper_2411_06360_b200/csrc/*.cuh) $(wildcard paper_2411_06360_b200/csrc/*.h) include/rsr_b200.h
 LIB := paper_2411_06360_b200/lib/librsr_b200.so
 OBJDIR := build/obj
 OBJ := $(patsubst paper_2411_06360_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
+# host-only C++ (session staging): AVX2 baseline like the oracle (x86-64-v3 runs on the GPU box)
+CXXSRC := $(wildcard paper_2411_06360_b200/csrc/*.cpp)
+CXXOBJ := $(patsubst paper_2411_06360_b200/csrc/%.cpp,$(OBJDIR)/%.cpp.o,$(CXXSRC))
+CXXFLAGS_HOST := -O3 -march=x86-64-v3 -fPIC -std=c++17 -Wall -Wextra
 
 PYINC := $(shell python3 -c "import sysconfig; print(sysconfig.get_paths()['include'])")
 PYEXT := paper_2411_06360_b200/lib/_rsrhost$(shell python3 -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
@@ -21,9 +25,13 @@ $(OBJDIR)/%.o: paper_2411_06360_b200/csrc/%.cu $(HDR)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
 
-$(LIB): $(OBJ)
+$(OBJDIR)/%.cpp.o: paper_2411_06360_b200/csrc/%.cpp $(HDR) $(wildcard paper_2411_06360_b200/csrc/*.h)
+	@mkdir -p $(OBJDIR)
+	g++ $(CXXFLAGS_HOST) -c $< -o $@
+
+$(LIB): $(OBJ) $(CXXOBJ)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -Xlinker -soname=librsr_b200.so -o $@ $(OBJ) -lcudart
+	$(NVCC) $(ARCH) -shared -Xlinker -soname=librsr_b200.so -o $@ $(OBJ) $(CXXOBJ) -lcudart
 
 oracle:
 	$(MAKE) -s -C oracle
@@ -36,6 +44,6 @@ clean:
 TRACE_LIB := paper_2411_06360_b200/lib/trace/librsr_b200_trace.so
 trace: $(SRC) $(HDR)
 	@mkdir -p $(dir $(TRACE_LIB))
-	$(NVCC) $(NVFLAGS) -DRSR_TRACE -shared -o $(TRACE_LIB) $(SRC) -lcudart
+	$(NVCC) $(NVFLAGS) -DRSR_TRACE -shared -o $(TRACE_LIB) $(SRC) $(CXXSRC) -lcudart
 
 .PHONY: all oracle clean trace

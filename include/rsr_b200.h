@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RSR_B200_ABI_VERSION 2
+#define RSR_B200_ABI_VERSION 3
 
 typedef enum rsr_status {
   RSR_OK = 0,
@@ -38,7 +38,7 @@ typedef enum rsr_status {
   RSR_ERR_CUDA = 3,        /* CUDA runtime failure */
 } rsr_status;
 
-typedef enum rsr_dtype { RSR_I32 = 0, RSR_F32 = 1, RSR_F64 = 2 } rsr_dtype;
+typedef enum rsr_dtype { RSR_I32 = 0, RSR_F32 = 1, RSR_F64 = 2, RSR_I64 = 3 } rsr_dtype;
 
 /* kernels.py:14-21 `_VARIANTS`: "rsr" -> dense block product, "rsrpp"/"rsr++" -> fold. */
 typedef enum rsr_variant { RSR_VARIANT_RSR = 0, RSR_VARIANT_RSRPP = 1 } rsr_variant;
@@ -159,28 +159,51 @@ rsr_status rsr_multiply_batched(const rsr_index_desc* desc, const void* V, rsr_d
                                 rsr_variant variant, void* workspace, size_t workspace_bytes,
                                 void* stream);
 
+/* Exact wide-integer multiply (int64 activations): the reference computes in fp64
+ * (core.py:110-117), exact for every integer vector whose partial sums stay below 2^53
+ * (SPEC.md:276), while int32 accumulation is exact only while sum_r |v_r| <= 2^31 - 1.  v is
+ * split into L balanced base-2^s digit vectors (rows * 2^(s-1) <= 2^31 - 1), each runs through
+ * the int32 multiply, and the limb results recombine in 128-bit integers (csrc/wide.cu).
+ * v: int64 [rows] (device); max_abs: a bound on |v| (0 = the whole int64 range; it sets L);
+ * out: [cols] int64 (wraps modulo 2^64) or float64 (the exact integer, rounded once); only the
+ * block range's columns are written.  workspace: rsr_multiply_wide_workspace_bytes() device
+ * bytes, 256-byte aligned. */
+size_t rsr_multiply_wide_workspace_bytes(const rsr_index_desc* desc, uint64_t max_abs);
+rsr_status rsr_multiply_wide(const rsr_index_desc* desc, const int64_t* v, uint64_t max_abs, void* out,
+                             rsr_dtype out_dtype, rsr_variant variant, int32_t block_begin, int32_t block_end,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
 /* End-to-end entry with HOST buffers (the call a reference-side binding makes):
  * copies v_host -> d_v, multiplies all blocks, copies d_out -> out_host and
  * synchronizes the stream.  d_v / d_out are caller-owned device scratch of the
- * right size; v_host / out_host should be pinned for async copies. */
+ * right size; v_host / out_host should be pinned for async copies.  int32 / float32 / float64
+ * vectors only, computed in that type (int32 wraps modulo 2^32: see the session below for the
+ * exact reference contract). */
 rsr_status rsr_multiply_host(const rsr_index_desc* desc, const void* v_host, rsr_dtype v_dtype,
                              void* out_host, rsr_dtype out_dtype, rsr_variant variant,
                              void* d_v, void* d_out, void* stream);
 
-/* Host-buffer session (the e2e call): pinned staging for v, a device copy of v and of the result,
- * and a mapped pinned result buffer, allocated once for one index and one vector type (int32,
- * fp32 or fp64) on the current device.  rsr_host_session_multiply replaces multiply_ternary /
- * multiply_rsr with host buffers (kernels.py:185-206): v_host [rows] of the session's type (any
- * host memory, v_bytes = its size) -> out_host [cols] of out_dtype (F64, the reference's result
- * type, or the vector type; out_bytes = its size).  It copies v into the staging buffer,
- * enqueues H2D(v) and the multiply (a single-split scatter launch stores its results straight
- * into the mapped buffer; other forms add a D2H copy), synchronizes the stream and converts the
- * result into out_host.  One call at a time per session (use one session per thread). */
+/* Host-buffer session (the e2e call `multiply_ternary(numpy v, idx)`, kernels.py:185-206):
+ * pinned staging, device copies of v and of the result, and mapped pinned result memory,
+ * allocated once for one index on the current device.  rsr_host_session_multiply takes v_host
+ * [rows] of any element type, v_bytes = its size, and writes out_host [cols] (out_bytes = its size)
+ * as float64 (the reference's result type) or as the vector type.  Staging classifies v in the
+ * same pass that copies it (csrc/host_stage.cpp), so the result is exact wherever the
+ * reference's fp64 result is:
+ *   - integer-valued v (int32 / int64, or float64 holding integers) with sum |v| <= 2^31 - 1:
+ *     int32 scatter multiply (bit-exact); the launch stores its results straight into the
+ *     mapped buffer (no D2H copy, no stream synchronize);
+ *   - other integer-valued v (|v| < 2^63): the exact wide multiply above;
+ *   - float32: fp32 (exact fixed-point scatter while rows <= 16384, else the gather kernel);
+ *   - other float64: the fp64 gather kernel.
+ * A non-finite entry fails with RSR_ERR_INVALID "vector entries must be finite" (core.py:115).
+ * out_dtype = int32 with int32 v keeps int32 arithmetic (modulo 2^32).  One call at a time per
+ * session (use one session per thread). */
 typedef struct rsr_host_session rsr_host_session;
-rsr_status rsr_host_session_create(const rsr_index_desc* desc, rsr_dtype v_dtype, rsr_host_session** out);
+rsr_status rsr_host_session_create(const rsr_index_desc* desc, rsr_host_session** out);
 void rsr_host_session_destroy(rsr_host_session* session);
-rsr_status rsr_host_session_multiply(rsr_host_session* session, const void* v_host, size_t v_bytes,
-                                     void* out_host, size_t out_bytes, rsr_dtype out_dtype,
+rsr_status rsr_host_session_multiply(rsr_host_session* session, const void* v_host, rsr_dtype v_dtype,
+                                     size_t v_bytes, void* out_host, rsr_dtype out_dtype, size_t out_bytes,
                                      rsr_variant variant, void* stream);
 /* Replaces segmented_sum / `_segment_sums` (kernels.py:50-60, 94-101): gather-form
  * bucket sums u[0..2^w) of one block of one half. */

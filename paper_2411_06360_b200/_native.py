@@ -14,18 +14,18 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RSR_B200_LIB") or os.path.join(_HERE, "lib", "librsr_b200.so")  # override: A/B builds
 
 RSR_OK, RSR_ERR_INVALID, RSR_ERR_UNSUPPORTED, RSR_ERR_CUDA = 0, 1, 2, 3
-I32, F32, F64 = 0, 1, 2
+I32, F32, F64, I64 = 0, 1, 2, 3
 VARIANT_RSR, VARIANT_RSRPP = 0, 1
 FORM_AUTO, FORM_SCATTER, FORM_GATHER = 0, 1, 2
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # Every symbol include/rsr_b200.h declares (tests check the .so exports them all).
 EXPORTS = (
     "rsr_b200_abi_version", "rsr_b200_last_error", "rsr_index_layout",
     "rsr_preprocess_workspace_bytes", "rsr_preprocess_ternary", "rsr_preprocess_binary",
     "rsr_index_import_workspace_bytes", "rsr_index_import",
-    "rsr_multiply", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host",
+    "rsr_multiply", "rsr_multiply_wide_workspace_bytes", "rsr_multiply_wide", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host",
     "rsr_host_session_create", "rsr_host_session_destroy", "rsr_host_session_multiply", "rsr_segmented_sum",
     "rsr_block_product", "rsr_naive_multiply_ternary",
     "rsr_dense_plane_words", "rsr_dense_pack_ternary", "rsr_dense_multiply",
@@ -78,6 +78,11 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, I32_, I32_, P]
     L.rsr_multiply.restype = st
+    L.rsr_multiply_wide_workspace_bytes.argtypes = [ctypes.POINTER(IndexDesc), ctypes.c_uint64]
+    L.rsr_multiply_wide_workspace_bytes.restype = SZ
+    L.rsr_multiply_wide.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_uint64, P, ctypes.c_int, ctypes.c_int,
+                                    I32_, I32_, P, SZ, P]
+    L.rsr_multiply_wide.restype = st
     L.rsr_index_import_workspace_bytes.argtypes = [ctypes.POINTER(IndexDesc)]
     L.rsr_index_import_workspace_bytes.restype = SZ
     L.rsr_index_import.argtypes = [ctypes.POINTER(IndexDesc), P, P, P, P, I64, P, SZ, P, P]
@@ -90,11 +95,11 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply_host.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                     ctypes.c_int, P, P, P]
     L.rsr_multiply_host.restype = st
-    L.rsr_host_session_create.argtypes = [ctypes.POINTER(IndexDesc), ctypes.c_int, ctypes.POINTER(P)]
+    L.rsr_host_session_create.argtypes = [ctypes.POINTER(IndexDesc), ctypes.POINTER(P)]
     L.rsr_host_session_create.restype = st
     L.rsr_host_session_destroy.argtypes = [P]
     L.rsr_host_session_destroy.restype = None
-    L.rsr_host_session_multiply.argtypes = [P, P, SZ, P, SZ, ctypes.c_int, ctypes.c_int, P]
+    L.rsr_host_session_multiply.argtypes = [P, P, ctypes.c_int, SZ, P, ctypes.c_int, SZ, ctypes.c_int, P]
     L.rsr_host_session_multiply.restype = st
     L.rsr_segmented_sum.argtypes = [ctypes.POINTER(IndexDesc), I32_, I32_, P, ctypes.c_int, P, P]
     L.rsr_segmented_sum.restype = st

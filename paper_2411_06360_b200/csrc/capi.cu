@@ -23,6 +23,9 @@ rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t ld
 rsr_status block_product(const double* u, int w, int use_fold, double* buf, double* out, cudaStream_t s);
 size_t batched_workspace_bytes(const rsr_index_desc& d, int64_t batch, rsr_dtype dt);
 size_t index_import_workspace_bytes(const rsr_index_desc* d);
+size_t wide_workspace_bytes(const rsr_index_desc& d, uint64_t max_abs);
+rsr_status multiply_wide(const rsr_index_desc& d, const int64_t* v, uint64_t max_abs, void* out, rsr_dtype ot,
+                         rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s);
 size_t dense_plane_words(int64_t rows, int64_t cols);
 rsr_status dense_pack_ternary(const int8_t* A, int64_t lda, int64_t rows, int64_t cols, uint32_t* P, uint32_t* N,
                               int32_t* bad, cudaStream_t s);
@@ -182,7 +185,24 @@ rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_d
   if (!v || !out) return fail(RSR_ERR_INVALID, "null vector or output");
   if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
     return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
+  if (v_dtype == RSR_I64) return fail(RSR_ERR_INVALID, "int64 activations go through rsr_multiply_wide");
   return multiply(*desc, v, v_dtype, out, out_dtype, variant, form, block_begin, block_end, (cudaStream_t)stream);
+}
+
+size_t rsr_multiply_wide_workspace_bytes(const rsr_index_desc* desc, uint64_t max_abs) {
+  return desc ? wide_workspace_bytes(*desc, max_abs) : 0;
+}
+
+rsr_status rsr_multiply_wide(const rsr_index_desc* desc, const int64_t* v, uint64_t max_abs, void* out,
+                             rsr_dtype out_dtype, rsr_variant variant, int32_t block_begin, int32_t block_end,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  rsr_status st = check_range(desc, block_begin, block_end);
+  if (st != RSR_OK) return st;
+  if (!v || !out) return fail(RSR_ERR_INVALID, "null vector or output");
+  if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
+    return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
+  return multiply_wide(*desc, v, max_abs, out, out_dtype, variant, block_begin, block_end, workspace, workspace_bytes,
+                       (cudaStream_t)stream);
 }
 
 size_t rsr_multiply_batched_workspace_bytes(const rsr_index_desc* desc, int64_t batch, rsr_dtype v_dtype) {
@@ -272,6 +292,7 @@ rsr_status rsr_multiply_host(const rsr_index_desc* desc, const void* v_host, rsr
   rsr_status st = check_range(desc, 0, desc ? desc->nblocks : 0);
   if (st != RSR_OK) return st;
   if (!v_host || !out_host || !d_v || !d_out) return fail(RSR_ERR_INVALID, "null buffer");
+  if (v_dtype == RSR_I64 || out_dtype == RSR_I64) return fail(RSR_ERR_INVALID, "rsr_multiply_host: int32, float32 or float64");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t vsz = v_dtype == RSR_F64 ? 8 : 4, osz = out_dtype == RSR_F64 ? 8 : 4;
   if ((st = cuda_check(cudaMemcpyAsync(d_v, v_host, desc->rows * vsz, cudaMemcpyHostToDevice, s), "H2D v")) != RSR_OK)

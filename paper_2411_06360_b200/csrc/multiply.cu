@@ -730,7 +730,7 @@ struct GatherParams {
 
 constexpr int kGatherWarps = 8;
 constexpr int kPermAhead = 4;  // perm windows in flight per warp (16-byte loads, registers)
-constexpr int kMaxWin = 64;    // windows per warp position range: rows <= 64 * 256 * ranges per half
+constexpr int kMaxWin = 64;    // window-end records buffered per warp (expanded when full)
 
 template <typename T>
 __device__ __forceinline__ T vload(const T* vs, const T* vg, uint32_t row, bool smem) {
@@ -904,6 +904,16 @@ __global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherP
               carry = (last_in >= 0) ? total - p_last : carry + total;
             }
             __syncwarp();
+            if (FOLDPP && nwin == kMaxWin) {  // record buffer full (long ranges): expand it now
+              for (int i = lane; i < nwin; i += 32) {
+                const int g = ebkt[i];
+                const T tt = etot[i];
+#pragma unroll
+                for (int s = 0; s < kMaxK; ++s) acc[s] += ((g >> s) & 1) ? tt : T(0);
+              }
+              nwin = 0;
+              __syncwarp();
+            }
           }
         }
       }
@@ -922,7 +932,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) gather_kernel(const GatherP
 #pragma unroll
       for (int s = kMaxK; s >= 0; --s) {
         const T bs = Bl[s];
-        if (s < kMaxK) acc[s] = suffix - bs;
+        if (s < kMaxK) acc[s] += suffix - bs;
         suffix += bs;
       }
       // window-end records, one per lane
@@ -1171,8 +1181,7 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
   const size_t max_smem = device_max_smem_optin();
   const size_t pbuf_bytes = sizeof(T) * (kGatherWarps * 256 + kGatherWarps * 16 + kGatherWarps * 32 * 17 +
                                          kGatherWarps * kMaxWin) + sizeof(int) * kGatherWarps * kMaxWin;
-  if (d.rows > (int64_t)kMaxWin * 256 * (kGatherWarps / d.halves))
-    return fail(RSR_ERR_UNSUPPORTED, "gather multiply supports at most 65536 (ternary) / 131072 (binary) rows");
+  if (d.rows > ((int64_t)1 << 30)) return fail(RSR_ERR_UNSUPPORTED, "gather multiply supports at most 2^30 rows");
   p.seg_in_smem = sizeof(uint32_t) * 2 * (size_t)((d.seg_stride + 3) & ~3) + pbuf_bytes <= (96u << 10);
   const size_t seg_words = p.seg_in_smem ? (size_t)((d.seg_stride + 3) & ~3) : 0;
   const size_t fixed = sizeof(uint32_t) * 2 * seg_words + pbuf_bytes;

@@ -1,16 +1,21 @@
 """Inference: segmented sums, block products and the fused multiply, on the GPU.
 
 Mirrors the reference `rsr.kernels` (kernels.py:1-239): same names, argument
-meanings, validation order and error messages.  Every multiply is one launch
-of the sm_100a kernels in librsr_b200.so (see csrc/multiply.cu):
+meanings, validation order and error messages.  Every multiply runs the sm_100a
+kernels in librsr_b200.so (see csrc/multiply.cu):
 
-* NumPy / list input keeps the reference contract (fp64 in, fp64 out).  The
-  call copies v to a pinned buffer, and one C-ABI call (`rsr_multiply_host`)
-  does H2D, the multiply and D2H.  fp64 vectors use the deterministic gather
-  kernel in fp64; integer-typed NumPy vectors use the int32 scatter kernel
-  (exact) and still return fp64.
-* torch CUDA tensors stay on the device: int32 -> int32 (scatter kernel, bit-
-  exact), float32 -> float32 and float64 -> float64 (gather kernel).
+* NumPy / list input keeps the reference contract (any real vector in, fresh fp64
+  out).  One host-buffer session call per multiply (rsr_host_session_multiply,
+  csrc/host.cu) stages v into pinned memory and classifies it in the same pass
+  (csrc/host_stage.cpp): integer-valued vectors (int32 / int64 / float64 holding
+  integers) run on the int32 scatter kernel when sum |v| <= 2^31 - 1 — bit-exact —
+  and on the exact wide multiply otherwise (csrc/wide.cu, limbs + int128
+  recombination), so the result equals the reference's fp64 result wherever that
+  one is exact; float32 vectors run in fp32 (exact fixed point);
+  other float64 vectors run on the fp64 gather kernel.
+* torch CUDA tensors stay on the device: int32 -> int32 (scatter kernel, int32
+  arithmetic modulo 2^32), int64 -> int64 (wide multiply, exact modulo 2^64),
+  float32 -> float32, float64 -> float64 (gather kernel).
 """
 
 from __future__ import annotations
@@ -150,11 +155,12 @@ _DTYPES = {}
 def _torch_dtype_code(t) -> int:
     import torch
     if not _DTYPES:
-        _DTYPES.update({torch.int32: _native.I32, torch.float32: _native.F32, torch.float64: _native.F64})
+        _DTYPES.update({torch.int32: _native.I32, torch.float32: _native.F32, torch.float64: _native.F64,
+                        torch.int64: _native.I64})
     try:
         return _DTYPES[t.dtype]
     except KeyError:
-        raise ValueError("device vectors must be int32, float32 or float64") from None
+        raise ValueError("device vectors must be int32, int64, float32 or float64") from None
 
 
 class _HostStaging(threading.local):
@@ -163,36 +169,26 @@ class _HostStaging(threading.local):
 
     def __init__(self):
         self.bufs = {}
-        self.plans = {}  # id(index) -> (weakref to the index, {kind: _HostPlan}); no strong refs
-
-    def get(self, key, shape, dtype, pinned):
-        """(tensor, numpy view or None, data pointer) of a cached buffer of `shape` elements."""
-        import torch
-        dev = -1 if pinned else torch.cuda.current_device()
-        ent = self.bufs.get((key, shape, dev))
-        if ent is None or ent[0].dtype != dtype:
-            t = (torch.empty(shape, dtype=dtype, pin_memory=True) if pinned
-                 else torch.empty(shape, dtype=dtype, device="cuda"))
-            ent = (t, t.numpy() if pinned else None, t.data_ptr())
-            self.bufs[(key, shape, dev)] = ent
-        return ent
+        self.plans = {}  # id(index) -> (weakref to the index, _HostPlan); no strong refs
 
 
 _staging = _HostStaging()
-_KIND_CODE = {"i32": _native.I32, "f32": _native.F32, "f64": _native.F64}
+_HOST_CODES = {np.dtype(np.int32): _native.I32, np.dtype(np.int64): _native.I64,
+               np.dtype(np.float32): _native.F32, np.dtype(np.float64): _native.F64}
+_I32_MAX = 2 ** 31 - 1
 
 
 class _HostPlan:
     """One host-buffer session (rsr_host_session_*: pinned staging, device scratch, mapped
-    result + completion flag) for one index, vector type and thread, created on first use and
-    destroyed with the index or the thread."""
+    result + completion flag) for one index and thread, created on first use and destroyed
+    with the index or the thread."""
     __slots__ = ("session", "cols", "call", "stream", "__weakref__")
 
-    def __init__(self, idx, kind):
+    def __init__(self, idx):
         import torch
         L = _native.lib()
         h = ctypes.c_void_p()
-        _native.check(L.rsr_host_session_create(ctypes.byref(idx.desc), _KIND_CODE[kind], ctypes.byref(h)))
+        _native.check(L.rsr_host_session_create(ctypes.byref(idx.desc), ctypes.byref(h)))
         self.session = h.value
         self.cols = idx.cols
         self.call = _native.host_ext().multiply
@@ -203,32 +199,85 @@ class _HostPlan:
         weakref.finalize(self, L.rsr_host_session_destroy, h.value)
 
 
-def _host_plan(idx, kind) -> _HostPlan:
+def _host_plan(idx) -> _HostPlan:
     plans = _staging.plans
     ent = plans.get(id(idx))
     if ent is None or ent[0]() is not idx:
         key = id(idx)
-        ent = plans[key] = (weakref.ref(idx, lambda _r, k=key, d=plans: d.pop(k, None)), {})
-    per = ent[1]
-    plan = per.get(kind)
-    if plan is None:
-        plan = per[kind] = _HostPlan(idx, kind)
-    return plan
+        ent = plans[key] = (weakref.ref(idx, lambda _r, k=key, d=plans: d.pop(k, None)), _HostPlan(idx))
+    return ent[1]
 
 
-def _run_host(idx, kind, v: np.ndarray, use_fold: bool) -> np.ndarray:
-    """One session call: v (C-contiguous, the session's type) -> fresh fp64 result (the
-    reference's result type)."""
-    plan = _host_plan(idx, kind)
+def _host_vector(v_in) -> np.ndarray:
+    """The vector as a C-contiguous 1-D int32 / int64 / float32 / float64 array with the
+    reference's value (`as_vector`, core.py:110-117, casts everything to float64: narrower
+    integer types widen losslessly; anything else takes that cast)."""
+    raw = v_in if type(v_in) is np.ndarray else np.asarray(v_in)
+    dt = raw.dtype
+    if dt in _HOST_CODES:
+        arr = raw
+    elif dt.kind == "b" or (dt.kind in "iu" and dt.itemsize < 4):  # bool, (u)int8, (u)int16
+        arr = raw.astype(np.int32)
+    elif dt == np.uint32 or (dt == np.uint64 and raw.size and int(raw.max()) < 2 ** 63):
+        arr = raw.astype(np.int64)
+    else:
+        arr = as_vector(raw)  # the reference's own cast and checks (float16, uint64 >= 2^63, ...)
+    if arr.ndim != 1 or arr.shape[0] < 1:
+        raise ValueError("vector must be 1-D with at least one entry")
+    return arr if arr.flags.c_contiguous else np.ascontiguousarray(arr)
+
+
+def _check_finite(arr: np.ndarray) -> None:
+    if arr.dtype.kind == "f" and not np.isfinite(arr).all():
+        raise ValueError("vector entries must be finite")
+
+
+def _check_length(arr: np.ndarray, rows: int) -> None:
+    if arr.shape[0] != rows:
+        _check_finite(arr)  # as_vector validates before the length check (kernels.py:188-190)
+        raise ValueError(f"vector length {arr.shape[0]} does not match {rows} rows")
+
+
+def classify_host_vector(arr: np.ndarray):
+    """(kind, array, max_abs): the computation csrc/host_stage.cpp picks for a host vector,
+    restated in NumPy for the paths that do not use a session (multiply_parallel).
+    kind "i32": integer-valued with sum |v| <= 2^31 - 1 (int32 kernel, bit-exact);
+    "wide": other integer-valued vectors with |v| < 2^63 (exact wide multiply);
+    "f32": float32; "f64": other float64."""
+    if arr.dtype == np.float32:
+        _check_finite(arr)
+        return "f32", arr, 0
+    if arr.dtype.kind == "f":
+        _check_finite(arr)
+        if not ((np.abs(arr) < 2.0 ** 63).all() and (arr == np.trunc(arr)).all()):
+            return "f64", arr, 0
+        arr = arr.astype(np.int64)
+    mx = max(abs(int(arr.min())), abs(int(arr.max())))
+    total = float(np.abs(arr.astype(np.float64)).sum())  # exact for sums below 2^53
+    if total <= _I32_MAX:
+        return "i32", arr.astype(np.int32), mx
+    return "wide", arr.astype(np.int64), mx
+
+
+def _run_host(idx, arr: np.ndarray, use_fold: bool) -> np.ndarray:
+    """One session call: host vector (int32 / int64 / float32 / float64) -> fresh fp64 result
+    (the reference's result type)."""
+    plan = _host_plan(idx)
     out = np.empty(plan.cols, np.float64)
-    st = plan.call(plan.session, v, out, _native.F64, _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR,
-                   plan.stream())
+    st = plan.call(plan.session, arr, _HOST_CODES[arr.dtype], out, _native.F64,
+                   _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, plan.stream())
     if st:
         _native.check(st)
     return out
 
 
-def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO):
+def _wide_workspace(idx, max_abs: int, device):
+    import torch
+    nbytes = _native.lib().rsr_multiply_wide_workspace_bytes(ctypes.byref(idx.desc), max_abs)
+    return torch.empty(max(1, (nbytes + 7) // 8), dtype=torch.int64, device=device), nbytes
+
+
+def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO, max_abs: int = 0):
     """Device-tensor path: v CUDA tensor [rows] -> CUDA tensor [cols]."""
     import torch
     code = _torch_dtype_code(v)
@@ -240,51 +289,39 @@ def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_n
     if out is None:
         out = torch.empty(idx.cols, dtype=v.dtype, device=v.device)
     b0, b1 = block_range if block_range is not None else (0, idx.desc.nblocks)
+    variant = _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR
+    if code == _native.I64:  # exact wide multiply (limbs through the int32 kernel)
+        ws, nbytes = _wide_workspace(idx, max_abs, v.device)
+        _native.check(_native.lib().rsr_multiply_wide(
+            ctypes.byref(idx.desc), v.data_ptr(), max_abs, out.data_ptr(), _torch_dtype_code(out), variant, b0, b1,
+            ws.data_ptr(), nbytes, _native.current_stream_ptr()))
+        return out
     _native.check(_native.lib().rsr_multiply(
         ctypes.byref(idx.desc), v.data_ptr(), code, out.data_ptr(), _torch_dtype_code(out),
-        _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, form, b0, b1,
-        _native.current_stream_ptr()))
+        variant, form, b0, b1, _native.current_stream_ptr()))
     return out
 
 
 def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray:
     """Host-buffer path (reference contract): NumPy in, fresh fp64 NumPy out, via one
-    rsr_multiply_host call (H2D + multiply + D2H + sync)."""
-    raw = np.asarray(v_in)
-    if raw.dtype.kind in "iub" and compute in (None, "int32"):
-        # integer activations (always finite): no float64 round trip, range check only
-        # for dtypes wider than int32
-        if raw.ndim != 1 or raw.shape[0] < 1:
-            raise ValueError("vector must be 1-D with at least one entry")
-        if raw.shape[0] != idx.rows:
-            raise ValueError(f"vector length {raw.shape[0]} does not match {idx.rows} rows")
-        if raw.dtype == np.int32:
-            return _run_host(idx, "i32", raw if raw.flags.c_contiguous else np.ascontiguousarray(raw), use_fold)
-        if raw.dtype.itemsize < 4 or (raw.min() >= -2 ** 31 and raw.max() < 2 ** 31):
-            return _run_host(idx, "i32", np.ascontiguousarray(raw, np.int32), use_fold)
-        if compute == "int32":
-            raise ValueError("integer activations exceed the int32 range")
-    if raw.dtype == np.float32 and compute in (None, "float32"):
-        # fp32 activations are computed in fp32 (north star: within 1e-5 relative of the
-        # fp64 reference); results come back as fresh fp64 arrays like the reference's
-        if raw.ndim != 1 or raw.shape[0] < 1:
-            raise ValueError("vector must be 1-D with at least one entry")
-        if not np.isfinite(raw).all():
-            raise ValueError("vector entries must be finite")
-        if raw.shape[0] != idx.rows:
-            raise ValueError(f"vector length {raw.shape[0]} does not match {idx.rows} rows")
-        return _run_host(idx, "f32", np.ascontiguousarray(raw), use_fold)
-    v = as_vector(v_in)
-    if v.shape[0] != idx.rows:
-        raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
+    host-buffer session call (stage + classify, H2D, multiply, result)."""
+    arr = _host_vector(v_in)
+    _check_length(arr, idx.rows)
+    if compute is None:
+        return _run_host(idx, arr, use_fold)
     if compute == "float32":
-        return _run_host(idx, "f32", v.astype(np.float32), use_fold)
+        _check_finite(arr)
+        return _run_host(idx, arr.astype(np.float32), use_fold)
     if compute == "int32":
-        if np.any(v != np.round(v)) or np.abs(v).max(initial=0) >= 2 ** 31:
-            raise ValueError("compute='int32' needs integer-valued activations in the int32 range")
-        return _run_host(idx, "i32", v.astype(np.int32), use_fold)
-    if compute in (None, "float64"):
-        return _run_host(idx, "f64", np.ascontiguousarray(v), use_fold)
+        kind, vv, _ = classify_host_vector(arr)
+        if kind != "i32":
+            raise ValueError("compute='int32' needs integer-valued activations with sum |v| <= 2^31 - 1")
+        return _run_host(idx, vv, use_fold)
+    if compute == "float64":  # the fp64 gather kernel, no integer routing
+        import torch
+        _check_finite(arr)
+        dv = torch.from_numpy(np.ascontiguousarray(arr, np.float64)).cuda()
+        return _multiply_device(dv, idx, use_fold).cpu().numpy()
     raise ValueError("compute must be int32, float32 or float64 for host vectors")
 
 
@@ -319,33 +356,43 @@ def multiply_parallel(v, idx, variant: str = "rsrpp", worker_count: int = 1, *, 
     """Blocks partitioned across workers, each writing a disjoint output slice
     (kernels.py:209-239).  Each worker's block range [i*nb//W, (i+1)*nb//W) is one
     block-range launch on the current stream (the same partition the multi-GPU
-    path shards across ranks); the result is bitwise independent of W."""
+    path shards across ranks); the result is bitwise independent of W.  Host vectors
+    take the same exact routing as multiply_ternary (classify_host_vector)."""
     import torch
     use_fold = _use_fold(variant)
     if worker_count < 1:
         raise ValueError("worker_count must be at least 1")
-    device_in = _is_device_tensor(v)
-    if device_in:
-        dv = v
-    else:
-        vv = as_vector(v)
-        if vv.shape[0] != idx.rows:
-            raise ValueError(f"vector length {vv.shape[0]} does not match {idx.rows} rows")
-        raw = np.asarray(v)
-        if compute == "int32" or (compute is None and raw.dtype.kind in "iub"):
-            dv = torch.from_numpy(vv.astype(np.int32)).cuda()
-        else:
-            dv = torch.from_numpy(vv).cuda()
-    if dv.shape[0] != idx.rows:
-        raise ValueError(f"vector length {dv.shape[0]} does not match {idx.rows} rows")
-    out_dtype = torch.float64 if (not device_in) else dv.dtype
-    out = torch.empty(idx.cols, dtype=out_dtype, device=dv.device)
     nb = idx.desc.nblocks
     bounds = [i * nb // worker_count for i in range(worker_count + 1)]
-    for lo, hi in zip(bounds, bounds[1:]):
-        if lo < hi:
-            _multiply_device(dv, idx, use_fold, (lo, hi), out)
-    return out if device_in else out.cpu().numpy()
+    ranges = [(lo, hi) for lo, hi in zip(bounds, bounds[1:]) if lo < hi]
+    if _is_device_tensor(v):
+        if v.shape[0] != idx.rows:
+            raise ValueError(f"vector length {v.shape[0]} does not match {idx.rows} rows")
+        out = torch.empty(idx.cols, dtype=v.dtype, device=v.device)
+        for r in ranges:
+            _multiply_device(v, idx, use_fold, r, out)
+        return out
+    arr = _host_vector(v)
+    _check_length(arr, idx.rows)
+    if compute == "float32":
+        kind, vv, mx = "f32", arr.astype(np.float32), 0
+    elif compute == "float64":
+        _check_finite(arr)
+        kind, vv, mx = "f64", arr.astype(np.float64), 0
+    elif compute in (None, "int32"):
+        kind, vv, mx = classify_host_vector(arr)
+        if compute == "int32" and kind != "i32":
+            raise ValueError("compute='int32' needs integer-valued activations with sum |v| <= 2^31 - 1")
+    else:
+        raise ValueError("compute must be int32, float32 or float64 for host vectors")
+    dv = torch.from_numpy(vv).cuda()
+    if kind == "f32":
+        out = torch.empty(idx.cols, dtype=torch.float32, device=dv.device)
+    else:  # int32 / wide / fp64 kernels write fp64 directly
+        out = torch.empty(idx.cols, dtype=torch.float64, device=dv.device)
+    for r in ranges:
+        _multiply_device(dv, idx, use_fold, r, out, max_abs=mx)
+    return out.double().cpu().numpy()
 
 
 def multiply_batched(V, idx, variant: str = "rsrpp"):
@@ -361,10 +408,13 @@ def multiply_batched(V, idx, variant: str = "rsrpp"):
         raise ValueError("V must be a CUDA tensor of shape [batch, rows]")
     V = V.contiguous()
     code = _torch_dtype_code(V)
+    if code == _native.I64:
+        raise ValueError("batched vectors must be int32, float32 or float64")
     out = torch.empty((V.shape[0], idx.cols), dtype=V.dtype, device=V.device)
     nbytes = _native.lib().rsr_multiply_batched_workspace_bytes(ctypes.byref(idx.desc), V.shape[0], code)
     # int64 elements: at least nbytes (allocations are 256-byte aligned)
-    ws = _staging.get("batch_ws", max(1, (nbytes + 7) // 8), torch.int64, False)[0] if nbytes else None
+    # per-call workspace from torch's stream-ordered caching allocator (never shared across streams)
+    ws = torch.empty(max(1, (nbytes + 7) // 8), dtype=torch.int64, device=V.device) if nbytes else None
     _native.check(_native.lib().rsr_multiply_batched(
         ctypes.byref(idx.desc), V.data_ptr(), code, V.shape[0], out.data_ptr(), code,
         _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR,

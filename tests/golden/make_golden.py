@@ -217,6 +217,31 @@ def counted() -> dict:
     return out
 
 
+def overflow() -> dict:
+    """Wide-value fixtures (tests/golden/overflow_inputs.py): integer activations whose column
+    sums exceed int32 (|v| = 2^20 at 16384 rows; int64 |v| up to 2^36 and 2^50),
+    float64 holding integers, high-dynamic-range floats, and 70000 rows.  The reference's
+    multiply_ternary / multiply_rsr (both variants) and multiply_parallel(W=3) on each; the
+    inputs are regenerated from their seeds by the tests (digests recorded here)."""
+    sys.path.insert(0, HERE)
+    from overflow_inputs import CASES, digest, make_inputs
+    out = {}
+    for name, (domain, rows, cols, k, kind, bound) in CASES.items():
+        A, v = make_inputs(name)
+        out[name + "_A_digest"] = np.array(digest(A))
+        out[name + "_v_digest"] = np.array(digest(v))
+        if domain == "ternary":
+            idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+            mult = rsr.multiply_ternary
+        else:
+            idx = rsr.preprocess(rsr.BinaryMatrix.from_dense(A.astype(np.uint8)), k)
+            mult = rsr.multiply_rsr
+        for variant in ("rsrpp", "rsr"):
+            out[f"{name}_{variant}"] = mult(v, idx, variant)
+        out[name + "_par3"] = rsr.multiply_parallel(v, idx, "rsrpp", 3)
+    return out
+
+
 def main() -> None:
     np.savez_compressed(os.path.join(HERE, "worked_example.npz"), **worked_example())
     np.savez_compressed(os.path.join(HERE, "fuzz_small.npz"), **fuzz_cases(101, 60, 64, 8))
@@ -225,6 +250,7 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "tuner.npz"), **tuner())
     np.savez_compressed(os.path.join(HERE, "rsx_products.npz"), **rsx_files())
     np.savez_compressed(os.path.join(HERE, "counted.npz"), **counted())
+    np.savez_compressed(os.path.join(HERE, "overflow.npz"), **overflow())
     print("reference rsr", rsr.__version__, "golden vectors written to", HERE)
 
 
