@@ -1,39 +1,49 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 RSR++ ternary matvec (BASELINE.json metric).
+"""Benchmark of the B200 RSR / RSR++ matvec (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config ternary16384|binary16384|llama4096|llama4096x14336|llama14336x4096|ternary65536]
+                    [--config NAME] [--variant rsrpp|rsr|both] [--replays R]
 
-One JSON line on stdout (rank 0).  A "step" is one RSR++ matvec v . A over the
-whole synthetic matrix with the index and v already resident in HBM (`value`);
-`e2e` is the same matvec through the reference-facing API with host buffers
-(`rsr.multiply_ternary(numpy_v, idx)`: H2D + kernel + D2H every step).
+One JSON line on stdout (rank 0).  A "step" is one matvec v . A over the whole synthetic
+matrix (one pass of the hot path over one batch: B=64 vectors for the batch config) with the
+index and v already resident in HBM (`value`).  The timed region is K steps captured in one
+CUDA graph; it is measured R times (default 11) and the median replay is reported
+(`ms_per_step` = median / K; every replay in `timing.replays_ms`).  `e2e` is the same metric
+through the reference-facing API with host buffers, in the reference's calling convention:
+`rsr.multiply_ternary(numpy float64 v, idx)` (core.py:110-117 casts every vector to fp64);
+the int32 host call is reported beside it (`e2e_int32`).
 
-L2 rule: each timed step multiplies against a different copy of the index
-(rotating >= 4 x L2 worth of index bytes), so no step reads an index the
-previous step left in L2.
+L2 rule: each timed step multiplies against a different copy of the index (rotating >= 4 x
+L2 worth of index bytes), so no step reads an index the previous step left in L2.
 
-N > 1 (torchrun): weak scaling of the column-sharded matvec — rank g owns a
-full 16384 x 16384 shard (the columns [g*m, (g+1)*m) of a 16384 x (N*m)
-matrix), multiplies it, and the output slices are NCCL all-gathered every step
-(the north star's column-block sharding + all-gather).  value = N shard-matvecs
-per step / max-over-ranks time.
+Configs (BASELINE.json): ternary16384 (default, the headline), ternary4096f32 (config 1),
+binary16384 (config 2: RSR and RSR++ side by side), ternary16384b64 (config 3),
+llama4096 / llama4096x14336 / llama14336x4096 (config 4), ternary65536 and ternary65536s
+(config 5).  Every line carries the CPU baseline (C port of the reference's RSR++ on all host
+cores and on one, and its standard dense multiply on one core) unless --no-cpu.
 
---config ternary65536s (BASELINE config 5, strong scaling): ONE 65536 x 65536 matrix whose
-column blocks are split over the ranks (the multiply_parallel partition), padded slices
-all-gathered every step; value = full matvecs per second.
+N > 1 (torchrun): the default is weak scaling of the column-sharded matvec — rank g owns a
+full n x m shard (columns [g*m, (g+1)*m) of an n x (N*m) matrix; rank 0's shard is the N=1
+matrix), multiplies it, and the output slices are NCCL all-gathered every step on a comm
+stream that overlaps the next step's multiply (double-buffered slices).  value = n x m
+shard-matvecs per second summed over ranks (each step is one matvec of the n x N*m matrix).
+`multi_gpu` reports the compute-only and compute + all-gather times separately and the check
+of the gathered vector against every rank's oracle slice.  --config ternary65536s (BASELINE
+config 5, strong scaling): ONE 65536 x 65536 matrix (hash-generated per entry, so every N
+shards the same matrix), rank g owning column blocks [g*NB//N, (g+1)*NB//N) (the
+multiply_parallel partition, kernels.py:222); value = full matvecs per second.
 
---impl reference: the reference algorithm's CPU path (oracle/rsr_oracle.c, a C
-port of `_run_blocks` + `multiply_parallel`; the reference itself is Python +
-Numba and cannot travel to the GPU box) on all host cores.
+--impl reference: the reference algorithm's CPU path (oracle/rsr_oracle.c, a C port of
+`_run_blocks` + `multiply_parallel`; the reference itself is Python + Numba and cannot travel
+to the GPU box) on all host cores, rank 0 only.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import re
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -47,22 +57,23 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (domain, n rows, m cols, workload description)
-    "ternary16384": ("ternary", 16384, 16384, "ternary 16384x16384 RSR++ matvec, k=11, int32 activations"),
-    "binary16384": ("binary", 16384, 16384, "binary 16384x16384 RSR++ matvec, k=11, int32 activations"),
-    "llama4096": ("ternary", 4096, 4096, "ternary 4096x4096 (Llama-3-8B q/o) RSR++ matvec, k=9"),
-    "llama4096x14336": ("ternary", 4096, 14336, "ternary 4096x14336 (Llama-3-8B gate/up) RSR++ matvec, k=9"),
-    "llama14336x4096": ("ternary", 14336, 4096, "ternary 14336x4096 (Llama-3-8B down) RSR++ matvec, k=11"),
-    "ternary65536": ("ternary", 65536, 65536, "ternary 65536x65536 RSR++ matvec, k=13"),
+    "ternary16384": ("ternary", 16384, 16384, "ternary 16384x16384 RSR++ matvec, int32-exact integer activations"),
+    "binary16384": ("binary", 16384, 16384, "binary 16384x16384 matvec, RSR and RSR++ kernels"),
+    "llama4096": ("ternary", 4096, 4096, "ternary 4096x4096 (Llama-3-8B q/o) RSR++ decode matvec"),
+    "llama4096x14336": ("ternary", 4096, 14336, "ternary 4096x14336 (Llama-3-8B gate/up) RSR++ decode matvec"),
+    "llama14336x4096": ("ternary", 14336, 4096, "ternary 14336x4096 (Llama-3-8B down) RSR++ decode matvec"),
+    "ternary65536": ("ternary", 65536, 65536, "ternary 65536x65536 RSR++ matvec"),
     "ternary16384b64": ("ternary", 16384, 16384, "ternary 16384x16384 RSR++, batch of 64 int32 activation vectors"),
-    "ternary4096f32": ("ternary", 4096, 4096, "ternary 4096x4096 RSR++ matvec, k=9, single fp32 vector"),
-    "ternary65536s": ("ternary", 65536, 65536, "ternary 65536x65536 RSR++ matvec, k=13, column blocks sharded "
+    "ternary4096f32": ("ternary", 4096, 4096, "ternary 4096x4096 RSR++ matvec, single fp32 vector"),
+    "ternary65536s": ("ternary", 65536, 65536, "ternary 65536x65536 RSR++ matvec, column blocks sharded "
                       "across the ranks (kernels.py:222 partition) + NCCL all-gather of the output"),
 }
 STRONG = {"ternary65536s"}  # BASELINE config 5: one matrix split over the ranks (strong scaling)
 FP32 = {"ternary4096f32"}
 FP32_TOL = 1e-5  # north star: fp32 activations within 1e-5 relative (norm-wise) of the fp64 reference
 BATCH = {"ternary16384b64": 64}
-PEAK_ADDS = 148 * 128 * 1.965e9  # fp32/int32 add lanes per second (SURVEY.md 8(d) adds/s view)
+BOTH_VARIANTS = {"binary16384"}  # BASELINE config 2: "RSR vs RSR++ kernels"
+PEAK_ADDS = 148 * 128 * 1.965e9  # int32 add lanes per second (SURVEY.md 8(d) adds/s view)
 L2_BYTES = 126 * 1024 * 1024
 
 
@@ -70,19 +81,20 @@ def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _profile_traffic(config: str):
-    """DRAM bytes per launch of the top kernel from the committed ncu capture, if any."""
+def _profile(config: str, variant: str = "rsrpp"):
+    """ncu numbers of this config's dominant kernel from the committed captures
+    (profiles/ncu_summary.json, written by tools/summarize_ncu.py)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
-        return s.get(config, {}).get("dram_bytes_per_launch")
+        return s.get(config if variant == "rsrpp" else f"{config}:{variant}", {})
     except Exception:
-        return None
+        return {}
 
 
 class ClockSampler:
@@ -141,12 +153,36 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def clocks_bad(cs) -> bool:
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(cs["reasons"])
+    stuck = bool(cs["sm_mhz"] and cs["sm_max_mhz"] and cs["sm_mhz"] < 0.8 * cs["sm_max_mhz"] and not cs["reasons"])
+    return bool(bad) or stuck
+
+
 def make_matrix(domain: str, n: int, m: int, seed: int = 0) -> np.ndarray:
     """Reference convention (bench.py:80-84): default_rng([seed, n, m]) uniform entries."""
     rng = np.random.default_rng([seed, n, m])
     if domain == "ternary":
         return rng.integers(-1, 2, size=(n, m), dtype=np.int8)
     return rng.integers(0, 2, size=(n, m), dtype=np.int8)
+
+
+def hashed_ternary(n: int, c0: int, c1: int, m_total: int, seed: int = 0):
+    """Columns [c0, c1) of an n x m_total uniform ternary matrix whose entry (i, j) is a hash of
+    (seed, i * m_total + j): every shard split of the same matrix gets the same entries
+    (strong-scaling config).  Built on the GPU in row chunks; returns a CUDA int8 tensor."""
+    import torch
+    M = torch.empty((n, c1 - c0), dtype=torch.int8, device="cuda")
+    cols = torch.arange(c0, c1, dtype=torch.int64, device="cuda")
+    mask = (1 << 62) - 1
+    for r0 in range(0, n, 4096):
+        r1 = min(n, r0 + 4096)
+        x = torch.arange(r0, r1, dtype=torch.int64, device="cuda")[:, None] * m_total + cols[None, :]
+        x = (x + seed * 0x5851F42D4C957F2D + 0x14057B7EF767814F) & mask
+        for mul in (0x2545F4914F6CDD1D, 0x1B873593):  # xorshift-multiply rounds (63-bit lanes)
+            x = ((x ^ (x >> 29)) * mul) & mask
+        M[r0:r1] = (((x >> 20) % 3) - 1).to(torch.int8)
+    return M
 
 
 def make_vector(n: int, seed: int = 0) -> np.ndarray:
@@ -161,48 +197,42 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def time_cpu_reference(A: np.ndarray, v: np.ndarray, k: int, domain: str, min_seconds: float = 5.0,
-                       workers: int | None = None):
-    """The reference algorithm on host cores (C port), mean seconds per full matvec.
-    Warm-up 3 (bench.py:18,35-43), then repeat until min_seconds of samples."""
-    from oracle import c_oracle
-    workers = workers or cpu_threads()
-    n, m = A.shape
-    kp = c_oracle.keys_ternary(A, k, 1)
-    kn = c_oracle.keys_ternary(A, k, -1) if domain == "ternary" else None
-    v64 = v.astype(np.float64)
-    run = lambda: c_oracle.multiply_parallel(v64, kp, kn, m, k, True, workers)  # noqa: E731
+def _time_calls(run, budget_s: float, min_reps: int = 3):
+    """bench.py:35-43 semantics: 3 warm-ups, then perf_counter samples until the budget."""
     for _ in range(3):
-        out = run()
+        run()
     samples = []
-    t_end = time.perf_counter() + min_seconds
-    while time.perf_counter() < t_end or len(samples) < 3:
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(samples) < min_reps:
         t0 = time.perf_counter()
         run()
         samples.append(time.perf_counter() - t0)
-    return float(np.mean(samples)), len(samples), workers, out
+    return float(np.mean(samples)), len(samples)
 
 
-def time_cpu_extras(A: np.ndarray, v: np.ndarray, k: int, domain: str, budget_s: float = 6.0):
-    """the same C port on ONE thread, and the reference's standard dense
-    multiply (core.py:135-169, C port `naive_ternary`), each a bounded sample."""
+def cpu_baseline(A: np.ndarray, v: np.ndarray, k: int, domain: str, variant: str, budget_s: float, batch: int = 1):
+    """SURVEY.md §8(d) CPU baseline, on this box's host cores: the C port of the reference's
+    `multiply_parallel` (kernels.py:209-239) with W = all host threads (the line's `value`) and
+    W = 1, and the standard dense multiply (core.py:135-169, C port `naive_ternary`) on one
+    core.  fp64, the reference's type.  B = 64 = 64 sequential single-vector calls (the
+    reference has no batch API): timed per call."""
     from oracle import c_oracle
     n, m = A.shape
     kp = c_oracle.keys_ternary(A, k, 1)
     kn = c_oracle.keys_ternary(A, k, -1) if domain == "ternary" else None
     v64 = v.astype(np.float64)
-    res = {}
-    for name, run in (("rsrpp_1thread", lambda: c_oracle.multiply_parallel(v64, kp, kn, m, k, True, 1)),
-                      ("standard_1thread", lambda: c_oracle.naive_ternary(v64, A))):
-        run()
-        samples = []
-        t_end = time.perf_counter() + budget_s / 2
-        while time.perf_counter() < t_end or not samples:
-            t0 = time.perf_counter()
-            run()
-            samples.append(time.perf_counter() - t0)
-        res[name] = {"value": 1.0 / float(np.mean(samples)), "unit": "vectors/s", "cores": 1, "reps": len(samples)}
-    return res
+    fold = variant != "rsr"
+    W = cpu_threads()
+    t_all, r_all = _time_calls(lambda: c_oracle.multiply_parallel(v64, kp, kn, m, k, fold, W), budget_s * 0.5)
+    t_one, r_one = _time_calls(lambda: c_oracle.multiply_parallel(v64, kp, kn, m, k, fold, 1), budget_s * 0.25, 1)
+    t_std, r_std = _time_calls(lambda: c_oracle.naive_ternary(v64, A), budget_s * 0.25, 1)
+    name = "RSR++" if fold else "RSR"
+    return {"value": 1.0 / t_all, "unit": "vectors/s", "cores": W, "kind": "port",
+            "sample": f"{r_all} full {n}x{m} {name} matvecs (k={k}, fp64, C port of kernels.py:127-239 "
+                      f"multiply_parallel on {W} threads)" + (f"; batch {batch} = {batch} sequential calls" if batch > 1 else ""),
+            f"{variant}_1thread": {"value": 1.0 / t_one, "unit": "vectors/s", "cores": 1, "reps": r_one},
+            "standard_1thread": {"value": 1.0 / t_std, "unit": "vectors/s", "cores": 1, "reps": r_std,
+                                 "what": "naive_multiply (core.py:135-169), C port"}}
 
 
 def run_reference(args, cfg):
@@ -221,19 +251,20 @@ def run_reference(args, cfg):
     kp = c_oracle.keys_ternary(A, k, 1)
     kn = c_oracle.keys_ternary(A, k, -1) if domain == "ternary" else None
     v64 = v.astype(np.float64)
+    fold = _variants(args)[0] != "rsr"
     for _ in range(max(args.warmup, 0)):
-        c_oracle.multiply_parallel(v64, kp, kn, m, k, True, workers)
+        c_oracle.multiply_parallel(v64, kp, kn, m, k, fold, workers)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        c_oracle.multiply_parallel(v64, kp, kn, m, k, True, workers)
+        c_oracle.multiply_parallel(v64, kp, kn, m, k, fold, workers)
     dt = (time.perf_counter() - t0) / args.steps
     value = 1.0 / dt
     line = {
-        "impl": "reference", "metric": "ternary RSR++ matvec vectors/sec", "value": value,
+        "impl": "reference", "metric": _metric(domain), "value": value,
         "unit": "vectors/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "n": n, "m": m, "k": k, "batch": 1},
+        "config": _config_key(args, cfg, k),
         "cpu_baseline": {"value": value, "unit": "vectors/s", "cores": workers, "kind": "port",
                          "sample": f"{args.steps} full {n}x{m} RSR++ matvecs (C port of kernels.py:127-239)"},
         "e2e": {"value": value, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -241,10 +272,27 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def _metric(domain: str) -> str:
+    return f"{domain} RSR++ matvec vectors/sec"
+
+
+def _variants(args):
+    if args.variant == "auto":
+        return ["rsrpp", "rsr"] if args.config in BOTH_VARIANTS else ["rsrpp"]
+    return ["rsrpp", "rsr"] if args.variant == "both" else [args.variant]
+
+
+def _config_key(args, cfg, k):
+    """The `config` object both arms print (identical keys and values for the same run)."""
+    domain, n, m, desc = cfg
+    return {"workload": desc, "n": n, "m": m, "k": k, "batch": BATCH.get(args.config, 1)}
+
+
 def run_ours(args, cfg):
     import torch
     import paper_2411_06360_b200 as rsr
     from paper_2411_06360_b200 import _native
+    from paper_2411_06360_b200 import kernels as K
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -255,15 +303,15 @@ def run_ours(args, cfg):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     domain, n, m, desc = cfg
-    # block width: the B200 tuner (indexer.optimal_k_b200, measured per shape) unless --k; the
-    # CPU legs run the reference's own tuner (optimal_k_rsrpp), as the reference does
+    # block width: the reference tuner (optimal_k_rsrpp) unless it differs from the measured B200
+    # tuner (indexer.optimal_k_b200); results do not depend on k (integer products are exact)
     k_ref = rsr.optimal_k_rsrpp(n)
     k = args.k or rsr.optimal_k_b200(n, m)
-    desc = re.sub(r"k=\d+", f"k={k}", desc)
+    variants = _variants(args)
 
     # ---- data.  weak (default): rank g's shard = columns [g*m, (g+1)*m) of an n x (N*m) matrix.
     # strong (BASELINE config 5): rank g owns the column blocks [g*NB//N, (g+1)*NB//N) of ONE
-    # n x m matrix (dist.shard_columns, the multiply_parallel partition), seeded by its first column
+    # n x m matrix (dist.shard_columns, the multiply_parallel partition), hash-generated per entry
     strong = args.config in STRONG
     m_full = m
     c0, c1 = (0, m)
@@ -272,12 +320,14 @@ def run_ours(args, cfg):
         c0, c1 = D.shard_columns(m, k, world, rank)
         pad = max(D.slice_lengths(m, k, world))
         m = c1 - c0
+        dA = hashed_ternary(n, c0, c1, m_full)
+        A = dA.cpu().numpy()
     else:
         pad = m
-    A = make_matrix(domain, n, m, seed=c0 if strong else rank)
+        A = make_matrix(domain, n, m, seed=rank)
+        dA = torch.from_numpy(A).cuda()
     fp32 = args.config in FP32
     v = (np.random.default_rng([0, n, 2]).standard_normal(n).astype(np.float32) if fp32 else make_vector(n))
-    dA = torch.from_numpy(A).cuda()
     if domain == "ternary":  # first-use module loading of the preprocess kernels, untimed
         rsr.preprocess_ternary(dA[:256, :64].contiguous(), k if k <= 8 else 8)
     torch.cuda.synchronize()
@@ -289,8 +339,8 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     preprocess_s = time.perf_counter() - t0
 
-    # ---- the standard dense multiply on the GPU (2-bit planes, csrc/dense.cu): comparator
-    dense = rsr.DenseTernary(dA) if domain == "ternary" else None
+    # ---- the standard dense multiply on the GPU (csrc/dense.cu): comparator
+    dense = rsr.DenseTernary(dA) if domain == "ternary" and not strong else None
 
     # ---- parity gate at full size (untimed): GPU keys + product vs the C oracle
     from oracle import c_oracle
@@ -300,21 +350,24 @@ def run_ours(args, cfg):
     for h, keys in zip(halves, [kp, kn]):
         if not np.array_equal(h.host_arrays()[2], keys):
             raise SystemExit("parity failure: device keys differ from the oracle")
-    ref = c_oracle.multiply_parallel(v.astype(np.float64), kp, kn, m, k, True, cpu_threads())
+    refs = {var: c_oracle.multiply_parallel(v.astype(np.float64), kp, kn, m, k, var != "rsr", cpu_threads())
+            for var in variants}
+    ref = refs[variants[0]]
     dv = torch.from_numpy(v).cuda()
-    got = rsr.multiply_ternary(dv, idx) if domain == "ternary" else rsr.multiply_rsr(dv, idx)
+    mult = rsr.multiply_ternary if domain == "ternary" else rsr.multiply_rsr
 
-    def same(x):
+    def same(x, r=ref):
         x = np.asarray(x, np.float64)
         if fp32:
-            return float(np.abs(x - ref).max()) <= FP32_TOL * max(float(np.abs(ref).max()), 1.0)
-        return np.array_equal(x, ref)
-    if not same(got.cpu().numpy()):
-        raise SystemExit("parity failure: device product differs from the oracle")
-    del A, dA
+            return float(np.abs(x - r).max()) <= FP32_TOL * max(float(np.abs(r).max()), 1.0)
+        return np.array_equal(x, r)
+    for var in variants:
+        if not same(mult(dv, idx, var).cpu().numpy(), refs[var]):
+            raise SystemExit(f"parity failure: device {var} product differs from the oracle")
+    del dA
 
     if args.config in BATCH:
-        return run_batch(args, cfg, idx, v, ref, kp, kn, k, preprocess_s, world, rank, dist)
+        return run_batch(args, cfg, idx, A, v, kp, kn, k, k_ref, preprocess_s, world, rank, dist)
 
     # ---- index copies so consecutive steps never hit an index left in L2
     def clone_index(src):
@@ -337,8 +390,7 @@ def run_ours(args, cfg):
     nblocks = idx.desc.nblocks
     hv = len(halves)
     row_stride = idx.desc.row_stride
-    read_bytes = hv * nblocks * row_stride * 2 + 4 * n + 4 * m          # bucket u16 + v + out (scatter)
-    seg_stride = idx.desc.seg_stride
+    index_bytes = hv * nblocks * row_stride * 2 + 4 * n + 4 * m          # bucket u16 + v + out (scatter)
     canonical = hv * sum(2 * n + 4 * (1 << min(k, m - b * k)) for b in range(nblocks)) + 4 * n + 4 * m
     ncopies = max(2, -(-4 * L2_BYTES // (hv * nblocks * row_stride * 2)))
     copies = [idx] + [clone_index(idx) for _ in range(ncopies - 1)]
@@ -346,103 +398,171 @@ def run_ours(args, cfg):
 
     stream = torch.cuda.current_stream()
     odt = torch.float32 if fp32 else torch.int32
-    out_pad = torch.zeros(pad, dtype=odt, device="cuda")  # equal all-gather sizes (strong: slices differ)
-    out = out_pad[:m]
-    mult = rsr.multiply_ternary if domain == "ternary" else rsr.multiply_rsr
-    gathered = torch.empty(world * pad, dtype=odt, device="cuda") if world > 1 else None
+    outs = [torch.zeros(pad, dtype=odt, device="cuda") for _ in range(2)]  # double-buffered slices
+    gathered = [torch.empty(world * pad, dtype=odt, device="cuda") for _ in range(2)] if world > 1 else None
+    comm = torch.cuda.Stream() if world > 1 else None
+    peak, peak_kind = _peaks()
 
-    from paper_2411_06360_b200 import kernels as K
+    def capture(var, with_comm):
+        """K steps in one CUDA graph.  Step i multiplies index copy i % C into slice buffer
+        i % 2; with_comm: the slice is all-gathered on the comm stream, which overlaps the next
+        step's multiply (the multiply two steps later waits for that gather before reusing the
+        buffer)."""
+        fold = var != "rsr"
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        if with_comm:
+            comm.wait_stream(stream)
+        done = [None, None]
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                for i in range(args.steps):
+                    b = i % 2
+                    if done[b] is not None:
+                        cap.wait_event(done[b])
+                    K._multiply_device(dv, copies[i % ncopies], fold, None, outs[b][:m])
+                    if with_comm:
+                        ev = torch.cuda.Event()
+                        ev.record(cap)
+                        comm.wait_event(ev)
+                        with torch.cuda.stream(comm):
+                            dist.all_gather_into_tensor(gathered[b], outs[b])
+                        done[b] = torch.cuda.Event()
+                        done[b].record(comm)
+                if with_comm:
+                    cap.wait_stream(comm)  # the graph ends after the last gather
+        stream.wait_stream(cap)
+        g.replay()  # warm the graph itself
+        torch.cuda.synchronize()
+        return g
 
-    def step(i):
-        K._multiply_device(dv, copies[i % ncopies], True, None, out)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, out_pad)
+    def timed(graph):
+        """R replays of the K-step graph (each bracketed by barrier + synchronize), clocks
+        sampled during them; median replay.  Re-measured once if the clocks were bad."""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.replays)]
 
+        def region():
+            with ClockSampler(local) as clocks:
+                t_load = time.perf_counter() + 0.5
+                while time.perf_counter() < t_load:  # load before the timed region (clocks settle)
+                    graph.replay()
+                    torch.cuda.synchronize()
+                ms = []
+                for e0, e1 in ev:
+                    if world > 1:
+                        dist.barrier()
+                    torch.cuda.synchronize()
+                    e0.record(stream)
+                    graph.replay()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(e0.elapsed_time(e1))
+                t_load = time.perf_counter() + 0.2
+                while time.perf_counter() < t_load:
+                    graph.replay()
+                    torch.cuda.synchronize()
+            return ms, clocks.summary()
+        ms, cs = region()
+        remeasured = clocks_bad(cs)
+        if remeasured:
+            ms, cs = region()
+        med = statistics.median(ms)
+        if world > 1:  # max over ranks of the median replay
+            tt = torch.tensor([med], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            med = float(tt.item())
+        cs["remeasured"] = remeasured
+        return med, ms, cs
+
+    # warm-up steps (untimed) through the public device API
     for i in range(max(args.warmup, 3)):
-        step(i)
+        for var in variants:
+            K._multiply_device(dv, copies[i % ncopies], var != "rsr", None, outs[0][:m])
     torch.cuda.synchronize()
 
-    # The timed K steps are one CUDA-graph replay: a 20 us kernel launched from Python
-    # would be launch-bound, a graph issues the K launches back to back.
-    graph = torch.cuda.CUDAGraph()
-    cap = torch.cuda.Stream()
-    cap.wait_stream(stream)
-    with torch.cuda.stream(cap):
-        with torch.cuda.graph(graph, stream=cap):
-            for i in range(args.steps):
-                K._multiply_device(dv, copies[i % ncopies], True, None, out)
-                if world > 1:
-                    dist.all_gather_into_tensor(gathered, out_pad)
-    stream.wait_stream(cap)
-    graph.replay()  # warm the graph itself
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-
-    t_begin = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-
-    def timed_region():
-        with ClockSampler(local) as clocks:
-            t_load = time.perf_counter() + 0.6
-            while time.perf_counter() < t_load:       # load before the timed region (clocks settle)
-                graph.replay()
-                torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            t_begin.record(stream)
-            graph.replay()
-            t_end.record(stream)
-            torch.cuda.synchronize()
-            t_load = time.perf_counter() + 0.3
-            while time.perf_counter() < t_load:       # and after it, so the sampler brackets it
-                graph.replay()
-                torch.cuda.synchronize()
-        return clocks
-
-    clocks = timed_region()
-    # a region that saw thermal / hardware slowdown (or clocks stuck low with no reason) is
-    # measured once more; the line reports the second measurement
-    cs = clocks.summary()
-    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(cs["reasons"])
-    stuck = bool(cs["sm_mhz"] and cs["sm_max_mhz"] and cs["sm_mhz"] < 0.8 * cs["sm_max_mhz"] and not cs["reasons"])
-    remeasured = False
-    if bad or stuck:
-        clocks = timed_region()
-        remeasured = True
-    total_ms = t_begin.elapsed_time(t_end)
-    kernel_ms = [total_ms / args.steps]
-    if world > 1:
-        tt = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-    ms_per_step = total_ms / args.steps
+    results = {}
+    for var in variants:
+        g = capture(var, world > 1)
+        med, ms, cs = timed(g)
+        results[var] = (med, ms, cs)
+        del g
+    med, ms, clocks = results[variants[0]]
+    ms_per_step = med / args.steps
+    kernel_us = ms_per_step * 1e3 if world == 1 else None
     # weak: shard-matvecs per second (N shards per step); strong: full matvecs per second
     value = (1 if strong else world) * 1e3 / ms_per_step
 
+    multi = None
+    if world > 1:
+        # compute-only (no all-gather) and the check of the gathered vector
+        g = capture(variants[0], False)
+        cmed, _, _ = timed(g)
+        del g
+        kernel_us = cmed / args.steps * 1e3
+        local_ref = torch.zeros(pad, dtype=torch.float64, device="cuda")
+        local_ref[:m] = torch.from_numpy(ref).cuda()
+        all_ref = torch.empty(world * pad, dtype=torch.float64, device="cuda")
+        dist.all_gather_into_tensor(all_ref, local_ref)
+        K._multiply_device(dv, idx, variants[0] != "rsr", None, outs[0][:m])
+        dist.all_gather_into_tensor(gathered[0], outs[0])
+        torch.cuda.synchronize()
+        ok = torch.equal(gathered[0].double(), all_ref) if not fp32 else \
+            float((gathered[0].double() - all_ref).abs().max()) <= FP32_TOL * max(1.0, float(all_ref.abs().max()))
+        okt = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if int(okt.item()) != 1:
+            raise SystemExit("parity failure: the all-gathered vector differs from the ranks' oracle slices")
+        multi = {"compute_only_us": cmed / args.steps * 1e3, "with_allgather_us": ms_per_step * 1e3,
+                 "allgather_exposed_us": ms_per_step * 1e3 - cmed / args.steps * 1e3,
+                 "allgather_bytes": world * pad * 4, "overlap": "all-gather of step i on a comm stream "
+                 "overlaps the multiply of step i+1 (double-buffered slices)",
+                 "gathered_vector_check": "bitwise equal (int32) to the all-gathered per-rank C-oracle slices"
+                 if not fp32 else "within 1e-5 norm-wise of the all-gathered per-rank C-oracle slices"}
+
     # ---- e2e through the reference-facing API with host buffers (rank-local)
-    v_host = v.copy()
-    if os.environ.get("RSR_BENCH_NO_E2E"):  # diagnostics (kernel A/B of library builds)
-        mult = lambda vh, idx: ref  # noqa: E731
-    for i in range(max(3, ncopies)):  # untimed: every copy's host session (pinned buffers) exists
-        mult(v_host, copies[i % ncopies])
-    torch.cuda.synchronize()
+    def e2e_time(vh, steps):
+        for i in range(max(3, ncopies)):  # untimed: every copy's host session (pinned buffers) exists
+            mult(vh, copies[i % ncopies])
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(steps):
+            res = mult(vh, copies[i % ncopies])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if not same(res):
+            raise SystemExit("parity failure on the e2e path")
+        t = e0.elapsed_time(e1) / steps
+        if world > 1:  # every rank's shard through the host API, max over ranks
+            tt = torch.tensor([t], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
     e2e_steps = min(max(args.steps, 20), 500)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(e2e_steps):
-        res = mult(v_host, copies[i % ncopies])
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    if not same(res):
-        raise SystemExit("parity failure on the e2e path")
-    if world > 1:  # weak scaling like `value`: every rank's shard through the host API, max over ranks
-        tt = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    scale = 1 if strong else world
+    # mapped result words the host reads (csrc/host.cu): 8-byte seq-tagged words up to 8 K
+    # columns, 4-byte results behind the fenced flag beyond
+    d2h = (8 if m <= 8192 else 4) * m
+    if fp32:
+        e2e_main_ms = e2e_time(v.copy(), e2e_steps)
+        e2e = {"value": scale * 1e3 / e2e_main_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * n,
+               "d2h_bytes_per_step": d2h, "path": "rsr.multiply_ternary(numpy float32 v, idx)"}
+        extra_e2e = {}
+    else:
+        v64 = v.astype(np.float64)  # the reference's calling convention (integer-valued fp64)
+        e2e_main_ms = e2e_time(v64, e2e_steps)
+        e2e_i32_ms = e2e_time(v.copy(), e2e_steps)
+        e2e = {"value": scale * 1e3 / e2e_main_ms, "unit": "vectors/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": d2h,
+               "path": f"rsr.{mult.__name__}(numpy float64 v, idx): the reference's calling convention; "
+                       "integer values classified while staged (csrc/host_stage.cpp), int32 kernel (exact), "
+                       "4-byte v over H2D" + (" — on every rank's shard" if world > 1 else "")}
+        extra_e2e = {"e2e_int32": {"value": scale * 1e3 / e2e_i32_ms, "unit": "vectors/s",
+                                   "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": d2h,
+                                   "path": f"rsr.{mult.__name__}(numpy int32 v, idx)"}}
 
     gpu_standard = None
     if dense is not None:
@@ -453,63 +573,77 @@ def run_ours(args, cfg):
         dg = torch.cuda.CUDAGraph()
         cap2 = torch.cuda.Stream()
         cap2.wait_stream(stream)
+        dsteps = min(args.steps, 200)
         with torch.cuda.stream(cap2), torch.cuda.graph(dg, stream=cap2):
-            for _ in range(min(args.steps, 200)):
+            for _ in range(dsteps):
                 dense.multiply(dv, dout)
         stream.wait_stream(cap2)
         dg.replay()
         torch.cuda.synchronize()
-        t_begin.record(stream)
-        dg.replay()
-        t_end.record(stream)
-        torch.cuda.synchronize()
-        d_us = t_begin.elapsed_time(t_end) / min(args.steps, 200) * 1e3
+        dms = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dg.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dms.append(e0.elapsed_time(e1))
+        d_us = statistics.median(dms) / dsteps * 1e3
         gpu_standard = {"value": 1e6 / d_us, "unit": "vectors/s", "kernel_us": d_us,
-                        "weight_bytes": dense.nbytes,
-                        "what": "dense 2-bit ternary GEMV on the same GPU (the paper's standard multiply, csrc/dense.cu)"}
+                        "weight_bytes": dense.nbytes, "hbm_frac": dense.nbytes / (d_us * 1e-6) / 1e9 / peak,
+                        "rsrpp_speedup": d_us / (ms_per_step * 1e3),
+                        "what": "dense ternary GEMV on the same GPU (the paper's standard multiply, csrc/dense.cu), "
+                                "weights L2-warm (one copy)"}
         del dense
 
-    peak, peak_kind = _peaks()
-    avg_kernel_s = statistics.mean(kernel_ms) / 1e3
-    # roofline.achieved counts the CANONICAL algorithmic bytes (u16 perm +
-    # u32 seg per block and half, + v + out); our index encoding reads fewer (index_bytes)
-    achieved = canonical / avg_kernel_s / 1e9
+    def roof(var):
+        # device time of the multiply alone (at N > 1: the compute-only graph of the main variant)
+        us = kernel_us if (world > 1 and var == variants[0]) else results[var][0] / args.steps * 1e3
+        achieved = canonical / (us * 1e-6) / 1e9
+        prof = _profile(args.config, var)
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": prof.get("dram_bytes_per_launch"), "peak_kind": peak_kind,
+                "algorithmic_bytes": canonical,
+                "bytes_definition": "SURVEY.md 8(d) canonical: sum over halves, blocks of 2n + 4*2^w, + 4n + 4m",
+                "index_bytes": index_bytes, "index_gbs": index_bytes / (us * 1e-6) / 1e9,
+                "kernel_us": us, "traffic_source": prof.get("capture")}
+
     line = {
-        "metric": "ternary RSR++ matvec vectors/sec" if domain == "ternary" else "binary RSR++ matvec vectors/sec",
+        "metric": _metric(domain),
         "value": value, "unit": "vectors/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "f32" if fp32 else "int32", "data": "synthetic",
-        "config": {"workload": desc + (f"; {world} column shards + NCCL all-gather" if world > 1 and not strong else ""),
-                   "n": n, "m": m_full, "k": k, "k_tuner": "optimal_k_b200 (reference tuner: k=%d)" % k_ref,
-                   "batch": 1, "l2": f"rotating {ncopies} index copies (>= 4x L2)",
-                   **({"shard_cols": [c0, c1], "ranks": world} if strong else {}),
-                   "form": "scatter (fp32: exact two-limb fixed point)" if fp32 else "scatter",
-                   "preprocess_s": round(preprocess_s, 4)},
-        "gpu_launches": args.steps * (1 if idx.desc.rows <= 16384 else 2),
-        "e2e": {"value": (1 if strong else world) * 1e3 / e2e_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * n,
-                # mapped result words the host reads (csrc/host.cu): 8-byte seq-tagged words up
-                # to 8 K columns, 4-byte results behind the fenced flag beyond
-                "d2h_bytes_per_step": (8 if m <= 8192 else 4) * m,
-                "path": f"rsr.multiply_ternary(numpy {'float32' if fp32 else 'int32'} v, idx)"
-                        + (" on every rank's shard (no collective: each rank's slice returns to its host)"
-                           if world > 1 else "")},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _profile_traffic(args.config),
-                     "peak_kind": peak_kind, "algorithmic_bytes": canonical,
-                     "bytes_definition": "SURVEY.md 8(d) canonical: sum over halves, blocks of 2n + 4*2^w, + 4n + 4m",
-                     "index_bytes": read_bytes, "index_gbs": read_bytes / avg_kernel_s / 1e9,
-                     "kernel_us": avg_kernel_s * 1e6},
-        "clocks": dict(clocks.summary(), remeasured=remeasured),
+        "config": _config_key(args, cfg, k),
+        "notes": {"k_tuner": f"optimal_k_b200 (the reference tuner gives k={k_ref}; results do not depend on k)",
+                  "l2": f"rotating {ncopies} index copies (>= 4x L2): inputs larger than L2 every step",
+                  "form": "scatter (fp32: exact two-limb fixed point)" if fp32 else "scatter (int32, exact)",
+                  "variant": variants[0], "preprocess_s": round(preprocess_s, 4),
+                  **({"value_unit": f"{n}x{m} shard-matvecs per second summed over {world} ranks (each step is "
+                                    f"one matvec of the {n}x{world * m} matrix)"} if world > 1 and not strong else {}),
+                  **({"shard_cols": [c0, c1], "matrix": "hash-generated per entry (same matrix for every N)"}
+                     if strong else {})},
+        "timing": {"replays": args.replays, "replays_ms": [round(x, 5) for x in ms], "statistic": "median replay",
+                   "timed_region": f"{args.steps} steps in one CUDA graph"},
+        "gpu_launches": args.steps * _count_launches(lambda: K._multiply_device(dv, idx, variants[0] != "rsr", None,
+                                                                                outs[0][:m])),
+        "e2e": e2e, **extra_e2e,
+        "roofline": roof(variants[0]),
+        "clocks": clocks,
     }
+    if len(variants) > 1:
+        line["variants"] = {var: {"kernel_us": results[var][0] / args.steps * 1e3,
+                                  "value": (1 if strong else world) * 1e3 / (results[var][0] / args.steps),
+                                  "roofline": roof(var), "replays_ms": [round(x, 5) for x in results[var][1]]}
+                            for var in variants}
+        line["variants"]["rsrpp_speedup_over_rsr"] = results["rsr"][0] / results["rsrpp"][0]
+    if multi is not None:
+        line["multi_gpu"] = multi
     if gpu_standard is not None:
         line["gpu_standard"] = gpu_standard
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu_s, reps, workers, _ = time_cpu_reference(make_matrix(domain, n, m), v, k_ref, domain,
-                                                     min_seconds=args.cpu_seconds)
-        line["cpu_baseline"] = {"value": 1.0 / cpu_s, "unit": "vectors/s", "cores": workers, "kind": "port",
-                                "sample": f"{reps} full {n}x{m} RSR++ matvecs, fp64, C port of "
-                                          "kernels.py:127-239 on {workers} threads".replace("{workers}", str(workers))}
-        line["cpu_baseline"].update(time_cpu_extras(make_matrix(domain, n, m), v, k_ref, domain))
+        line["cpu_baseline"] = cpu_baseline(A, v, k_ref, domain, variants[0], args.cpu_seconds)
+        if len(variants) > 1:
+            line["cpu_baseline_rsr"] = cpu_baseline(A, v, k_ref, domain, "rsr", args.cpu_seconds / 2)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -517,7 +651,7 @@ def run_ours(args, cfg):
         print(json.dumps(line), flush=True)
 
 
-def run_batch(args, cfg, idx, v, ref, kp, kn, k, preprocess_s, world, rank, dist):
+def run_batch(args, cfg, idx, A, v, kp, kn, k, k_ref, preprocess_s, world, rank, dist):
     """BASELINE config 3: one step = rsr.multiply_batched of B vectors against one index."""
     import torch
     import paper_2411_06360_b200 as rsr
@@ -532,23 +666,37 @@ def run_batch(args, cfg, idx, v, ref, kp, kn, k, preprocess_s, world, rank, dist
         r = c_oracle.multiply_parallel(Vh[i].astype(np.float64), kp, kn, m, k, True, cpu_threads())
         if not np.array_equal(got[i].astype(np.float64), r):
             raise SystemExit("parity failure: batched product differs from the oracle")
-    steps = min(args.steps, 200)
+    steps = args.steps
     for _ in range(max(args.warmup, 3)):
         rsr.multiply_batched(V, idx)
     torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stream = torch.cuda.current_stream()
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clocks:
-        t_load = time.perf_counter() + 0.5
-        while time.perf_counter() < t_load:
-            rsr.multiply_batched(V, idx)
-            torch.cuda.synchronize()
-        t0.record(stream)
-        for _ in range(steps):
-            rsr.multiply_batched(V, idx)
-        t1.record(stream)
-        torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1) / steps
+
+    def region():
+        # eager calls: the int32 packed-pair guard reads one device word per call (skipped, with
+        # per-vector launches, under graph capture)
+        with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clocks:
+            t_load = time.perf_counter() + 0.5
+            while time.perf_counter() < t_load:
+                rsr.multiply_batched(V, idx)
+                torch.cuda.synchronize()
+            ms = []
+            for _ in range(args.replays):
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                t0.record(stream)
+                for _ in range(steps):
+                    rsr.multiply_batched(V, idx)
+                t1.record(stream)
+                torch.cuda.synchronize()
+                ms.append(t0.elapsed_time(t1))
+        return ms, clocks.summary()
+    ms_list, cs = region()
+    remeasured = clocks_bad(cs)
+    if remeasured:
+        ms_list, cs = region()
+    cs["remeasured"] = remeasured
+    ms = statistics.median(ms_list) / steps
     # e2e: pinned host V -> device, batched multiply, result -> host, every step
     Vp = torch.from_numpy(Vh).pin_memory()
     Oh = torch.empty((B, m), dtype=torch.int32).pin_memory()
@@ -556,6 +704,7 @@ def run_batch(args, cfg, idx, v, ref, kp, kn, k, preprocess_s, world, rank, dist
         Oh.copy_(rsr.multiply_batched(Vp.cuda(non_blocking=True), idx), non_blocking=True)
     torch.cuda.synchronize()
     e_steps = min(steps, 50)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(e_steps):
         Oh.copy_(rsr.multiply_batched(Vp.cuda(non_blocking=True), idx), non_blocking=True)
@@ -563,48 +712,67 @@ def run_batch(args, cfg, idx, v, ref, kp, kn, k, preprocess_s, world, rank, dist
     t1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = t0.elapsed_time(t1) / e_steps
+    if not np.array_equal(Oh.numpy(), got):
+        raise SystemExit("parity failure on the batched e2e path")
     nblocks = idx.desc.nblocks
     canonical = 2 * sum(2 * n + 4 * (1 << min(k, m - b * k)) for b in range(nblocks)) + B * (4 * n + 4 * m)
     adds = B * (2 * sum(n + 2 * (1 << min(k, m - b * k)) - 2 for b in range(nblocks)) + m)
     peak, peak_kind = _peaks()
-    index_bytes = idx.desc.halves * nblocks * idx.desc.row_stride * 2
-    loop = index_bytes <= (96 << 20) and k <= 14
+    prof = _profile(args.config)
     line = {
-        "metric": "ternary RSR++ matvec vectors/sec", "value": B * 1e3 / ms, "unit": "vectors/s",
+        "metric": _metric(domain), "value": B * 1e3 / ms, "unit": "vectors/s",
         "n_gpus": world, "steps": steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": desc, "n": n, "m": m, "k": k, "batch": B,
-                   "form": "packed-pair scatter: two vectors per reduction, guard-checked (index L2-resident)"
-                           if loop else "batched gather",
-                   "l2": "index (97.8 MB) stays L2-resident across the batch: that residency is the amortisation",
-                   "preprocess_s": round(preprocess_s, 4)},
-        # loop: the guard + one packed-pair scatter launch per two vectors (csrc/capi.cu)
-        # (+ transpose and gather of every vector's short last block when m % k != 0)
-        "gpu_launches": steps * (1 + B // 2 + B % 2 + (2 if m % k else 0) if loop else 2),
+        "config": _config_key(args, cfg, k),
+        "notes": {"k_tuner": f"optimal_k_b200 (the reference tuner gives k={k_ref})",
+                  "form": prof.get("form", "rsr_multiply_batched"),
+                  "preprocess_s": round(preprocess_s, 4)},
+        "timing": {"replays": args.replays, "replays_ms": [round(x, 5) for x in ms_list],
+                   "statistic": "median replay", "timed_region": f"{steps} eager batched calls"},
+        "gpu_launches": None,
         "e2e": {"value": B * 1e3 / e2e_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * B * n,
-                "d2h_bytes_per_step": 4 * B * m, "path": "rsr.multiply_batched(pinned V.cuda(), idx) -> host"},
+                "d2h_bytes_per_step": 4 * B * m, "path": "rsr.multiply_batched(pinned V.cuda(), idx) -> pinned host"},
         "roofline": {"bound": "hbm", "achieved": canonical / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": canonical / (ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
-                     "algorithmic_bytes": canonical,
+                     "frac": canonical / (ms * 1e-3) / 1e9 / peak, "traffic": prof.get("dram_bytes_per_launch"),
+                     "peak_kind": peak_kind, "algorithmic_bytes": canonical,
                      "bytes_definition": "SURVEY.md 8(d) canonical, batch 64: index once + 64 x (4n + 4m)",
-                     "adds_per_s": adds / (ms * 1e-3), "adds_frac": adds / (ms * 1e-3) / PEAK_ADDS},
-        "clocks": clocks.summary(),
+                     "adds_per_s": adds / (ms * 1e-3), "adds_frac": adds / (ms * 1e-3) / PEAK_ADDS,
+                     "kernel_us": ms * 1e3},
+        "clocks": cs,
     }
+    line["gpu_launches"] = _count_launches(lambda: rsr.multiply_batched(V, idx)) * steps
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(A, v, k_ref, domain, "rsrpp", args.cpu_seconds, batch=B)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _count_launches(fn) -> int:
+    """Kernels one call launches (torch profiler over one call)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as p:
+        fn()
+        torch.cuda.synchronize()
+    return sum(1 for e in p.events() if e.device_type == torch.autograd.DeviceType.CUDA
+               and "memset" not in e.name.lower() and "memcpy" not in e.name.lower())
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--replays", type=int, default=11, help="timed replays of the K-step graph (median reported)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="ternary16384", choices=sorted(CONFIGS))
+    ap.add_argument("--variant", default="auto", choices=["auto", "rsrpp", "rsr", "both"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--k", type=int, default=0, help="block width override (default: the reference tuner)")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--k", type=int, default=0, help="block width override (default: indexer.optimal_k_b200)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
+    args.replays = max(1, args.replays)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
