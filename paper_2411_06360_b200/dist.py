@@ -32,19 +32,25 @@ def slice_lengths(cols: int, k: int, world: int) -> list[int]:
 
 
 def gather_output(local_out, cols: int, k: int, group=None):
-    """All-gather the ranks' output slices into the full [cols] vector (torch tensors on
-    the backend's device: CUDA for NCCL, CPU for gloo)."""
+    """All-gather the ranks' output slices into the full [cols] vector.  NCCL gathers CUDA
+    tensors in place (NVLink); a gloo group (CPU tests, or ranks sharing one GPU) gathers
+    CPU copies and the result comes back on local_out's device."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     lens = slice_lengths(cols, k, world)
     pad = max(lens)
-    send = torch.zeros(pad, dtype=local_out.dtype, device=local_out.device)
-    send[: local_out.numel()] = local_out
-    recv = torch.empty(world * pad, dtype=local_out.dtype, device=local_out.device)
+    if local_out.numel() != lens[dist.get_rank(group)]:
+        raise ValueError(f"local slice has {local_out.numel()} columns, the partition gives this rank "
+                         f"{lens[dist.get_rank(group)]}")
+    dev = local_out.device
+    comm_dev = torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
+    send = torch.zeros(pad, dtype=local_out.dtype, device=comm_dev)
+    send[: local_out.numel()] = local_out.to(comm_dev)
+    recv = torch.empty(world * pad, dtype=local_out.dtype, device=comm_dev)
     dist.all_gather_into_tensor(recv, send, group=group)
     parts = [recv[r * pad: r * pad + lens[r]] for r in range(world)]
-    return torch.cat(parts)
+    return torch.cat(parts).to(dev)
 
 
 def preprocess_ternary_shard(A, k: int, world: int, rank: int):
@@ -69,7 +75,11 @@ def preprocess_ternary_shard(A, k: int, world: int, rank: int):
 
 def multiply_sharded(v, local_idx, cols: int, group=None, variant: str = "rsrpp"):
     """v (CUDA tensor, full length rows) times the sharded matrix: local multiply of this
-    rank's blocks, then all-gather of the slices.  Returns the full [cols] CUDA tensor."""
-    from .kernels import multiply_ternary
-    local = multiply_ternary(v, local_idx, variant)
+    rank's blocks (one launch, its disjoint output slice), then all-gather of the slices.
+    Returns the full [cols] tensor on v's device; bitwise equal to the unsharded
+    multiply_ternary / multiply_rsr and to the reference's multiply_parallel(W=world)."""
+    from .indexer import TernaryIndex
+    from .kernels import multiply_rsr, multiply_ternary
+    mult = multiply_ternary if isinstance(local_idx, TernaryIndex) else multiply_rsr
+    local = mult(v, local_idx, variant)
     return gather_output(local, cols, local_idx.k, group)

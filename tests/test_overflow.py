@@ -167,4 +167,4 @@ def test_float32_high_dynamic_range(rsr, cuda, ov):
     print(f"fp32 HDR: max elementwise error / condition = {elem.max():.3e}, "
           f"norm-wise = {np.abs(got - ref).max() / np.abs(ref).max():.3e}")
     assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
-    assert elem.max() <= 1e-6
+    assert elem.max() <= 1e-7  # measured 1.9e-8 on the B200
