@@ -173,6 +173,52 @@ rsr_status rsr_multiply_wide(const rsr_index_desc* desc, const int64_t* v, uint6
                              rsr_dtype out_dtype, rsr_variant variant, int32_t block_begin, int32_t block_end,
                              void* workspace, size_t workspace_bytes, void* stream);
 
+/* Batch plan: the index re-cut for the batch-native kernel (BASELINE config 3, many vectors
+ * against one index; the reference has no batch API and runs `multiply_ternary`,
+ * kernels.py:196-206, once per vector).  The batch kernel's lanes span the VECTOR dimension:
+ * lane w owns the packed int16 pair of vectors 2w, 2w+1 (v + v' * 2^16), so one shared-memory
+ * reduction adds a row's 64 activations into the 32 consecutive words of ONE histogram slot —
+ * conflict-free, where the per-vector kernel's 32 random rows are not.  A slot is 128 bytes,
+ * so the plan uses narrower column blocks (kb, 9 at 16384 rows) than the index, and every
+ * row's bin becomes a SLOT: bins whose rows (both halves) could exceed int16 for |v| <= vmax
+ * are split into several slots (rows dealt round-robin by rank), so every slot's sum fits
+ * int16 and the packed accumulation is exact; the fold adds a split bin's slots back
+ * together in int32.  Built on the device from any index (perm + seg) by
+ * rsr_batch_plan_build; `extra` (the largest number of split slots of a unit) is read back
+ * once, at build time. */
+typedef struct rsr_batch_plan {
+  int64_t rows, cols;
+  int32_t kb;          /* plan block width */
+  int32_t nblocks;     /* ceil(cols / kb) */
+  int32_t halves;      /* 1 binary, 2 ternary */
+  int32_t split_rows;  /* rows per unit (multiple of 8); units = (plan block, row split) */
+  int32_t nsplits;     /* ceil(rows / split_rows) */
+  int32_t extra_cap;   /* entries per unit in slot_bins (split slots follow the unit's 2^w direct slots) */
+  int32_t extra;       /* histogram slots beyond 2^kb the widest unit needs (set by rsr_batch_plan_build) */
+  int32_t vmax;        /* packed form valid for |v| <= vmax (else int32 lanes, 32 vectors per pass) */
+  int64_t row_stride;  /* nsplits * split_rows */
+  uint16_t* codes;     /* [halves][nblocks][row_stride]: 4 * slot of each row (the slot's byte offset
+                          in a lane's histogram row; slot 0 = logical bin 0, never read) */
+  uint16_t* slot_bins; /* [nblocks * nsplits][extra_cap]: logical bin of split slot 2^w + e (0 ends the list) */
+} rsr_batch_plan;
+
+/* Fill the plan's size fields for an index (pointers untouched) and the device bytes of its
+ * arrays; RSR_ERR_UNSUPPORTED when the batch kernel does not apply (e.g. k < 2). */
+rsr_status rsr_batch_plan_layout(const rsr_index_desc* desc, rsr_batch_plan* plan, size_t* code_bytes,
+                                 size_t* map_bytes, size_t* workspace_bytes);
+/* Build the plan's arrays from the index (device kernels, then ONE host synchronisation of
+ * `stream` to read `extra`); RSR_ERR_UNSUPPORTED if a unit needs more split slots than fit. */
+rsr_status rsr_batch_plan_build(const rsr_index_desc* desc, rsr_batch_plan* plan, void* workspace,
+                                size_t workspace_bytes, void* stream);
+/* Batch-native multiply through a plan: V int32 [batch][rows] -> OUT int32 [batch][cols]
+ * (int32 arithmetic, exact modulo 2^32 like rsr_multiply).  No host synchronisation (CUDA
+ * graph capturable): a device flag picks the packed form (max |V| <= vmax) or int32 lanes.
+ * workspace: rsr_multiply_batched_plan_workspace_bytes() device bytes, 256-byte aligned. */
+size_t rsr_multiply_batched_plan_workspace_bytes(const rsr_batch_plan* plan, int64_t batch);
+rsr_status rsr_multiply_batched_plan(const rsr_index_desc* desc, const rsr_batch_plan* plan, const int32_t* V,
+                                     int64_t batch, int32_t* OUT, rsr_variant variant, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+
 /* End-to-end entry with HOST buffers (the call a reference-side binding makes):
  * copies v_host -> d_v, multiplies all blocks, copies d_out -> out_host and
  * synchronizes the stream.  d_v / d_out are caller-owned device scratch of the

@@ -29,6 +29,8 @@ EXPORTS = (
     "rsr_host_session_create", "rsr_host_session_destroy", "rsr_host_session_multiply", "rsr_segmented_sum",
     "rsr_block_product", "rsr_naive_multiply_ternary",
     "rsr_dense_plane_words", "rsr_dense_pack_ternary", "rsr_dense_multiply",
+    "rsr_batch_plan_layout", "rsr_batch_plan_build", "rsr_multiply_batched_plan_workspace_bytes",
+    "rsr_multiply_batched_plan",
 )
 
 
@@ -43,6 +45,16 @@ class IndexDesc(ctypes.Structure):
         ("perm_bytes", ctypes.c_int32), ("halves", ctypes.c_int32),
         ("row_stride", ctypes.c_int64), ("seg_stride", ctypes.c_int64),
         ("half", HalfIndex * 2),
+    ]
+
+
+class BatchPlan(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+        ("kb", ctypes.c_int32), ("nblocks", ctypes.c_int32), ("halves", ctypes.c_int32),
+        ("split_rows", ctypes.c_int32), ("nsplits", ctypes.c_int32), ("extra_cap", ctypes.c_int32),
+        ("extra", ctypes.c_int32), ("vmax", ctypes.c_int32), ("row_stride", ctypes.c_int64),
+        ("codes", ctypes.c_void_p), ("slot_bins", ctypes.c_void_p),
     ]
 
 
@@ -113,6 +125,16 @@ def lib() -> ctypes.CDLL:
     L.rsr_dense_multiply.restype = st
     L.rsr_naive_multiply_ternary.argtypes = [P, I64, I64, I64, P, ctypes.c_int, P, P]
     L.rsr_naive_multiply_ternary.restype = st
+    L.rsr_batch_plan_layout.argtypes = [ctypes.POINTER(IndexDesc), ctypes.POINTER(BatchPlan), ctypes.POINTER(SZ),
+                                        ctypes.POINTER(SZ), ctypes.POINTER(SZ)]
+    L.rsr_batch_plan_layout.restype = st
+    L.rsr_batch_plan_build.argtypes = [ctypes.POINTER(IndexDesc), ctypes.POINTER(BatchPlan), P, SZ, P]
+    L.rsr_batch_plan_build.restype = st
+    L.rsr_multiply_batched_plan_workspace_bytes.argtypes = [ctypes.POINTER(BatchPlan), I64]
+    L.rsr_multiply_batched_plan_workspace_bytes.restype = SZ
+    L.rsr_multiply_batched_plan.argtypes = [ctypes.POINTER(IndexDesc), ctypes.POINTER(BatchPlan), P, I64, P,
+                                            ctypes.c_int, P, SZ, P]
+    L.rsr_multiply_batched_plan.restype = st
     if L.rsr_b200_abi_version() != ABI_VERSION:
         raise ImportError("librsr_b200.so ABI version mismatch; rebuild with `make`")
     _lib = L

@@ -24,6 +24,12 @@ rsr_status block_product(const double* u, int w, int use_fold, double* buf, doub
 size_t batched_workspace_bytes(const rsr_index_desc& d, int64_t batch, rsr_dtype dt);
 size_t index_import_workspace_bytes(const rsr_index_desc* d);
 size_t wide_workspace_bytes(const rsr_index_desc& d, uint64_t max_abs);
+rsr_status batch_plan_layout(const rsr_index_desc& d, rsr_batch_plan* pl, size_t* code_bytes, size_t* map_bytes,
+                             size_t* ws_bytes);
+rsr_status batch_plan_build(const rsr_index_desc& d, rsr_batch_plan* pl, void* ws, size_t ws_bytes, cudaStream_t s);
+size_t batched_plan_workspace_bytes(const rsr_batch_plan& pl, int64_t batch);
+rsr_status multiply_batched_plan(const rsr_index_desc& d, const rsr_batch_plan& pl, const int32_t* V, int64_t batch,
+                                 int32_t* out, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s);
 rsr_status multiply_wide(const rsr_index_desc& d, const int64_t* v, uint64_t max_abs, void* out, rsr_dtype ot,
                          rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s);
 size_t dense_plane_words(int64_t rows, int64_t cols);
@@ -203,6 +209,39 @@ rsr_status rsr_multiply_wide(const rsr_index_desc* desc, const int64_t* v, uint6
     return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
   return multiply_wide(*desc, v, max_abs, out, out_dtype, variant, block_begin, block_end, workspace, workspace_bytes,
                        (cudaStream_t)stream);
+}
+
+rsr_status rsr_batch_plan_layout(const rsr_index_desc* desc, rsr_batch_plan* plan, size_t* code_bytes,
+                                 size_t* map_bytes, size_t* workspace_bytes) {
+  rsr_status st = check_range(desc, 0, desc ? desc->nblocks : 0);
+  if (st != RSR_OK) return st;
+  if (!plan) return fail(RSR_ERR_INVALID, "null plan");
+  return batch_plan_layout(*desc, plan, code_bytes, map_bytes, workspace_bytes);
+}
+
+rsr_status rsr_batch_plan_build(const rsr_index_desc* desc, rsr_batch_plan* plan, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  rsr_status st = check_range(desc, 0, desc ? desc->nblocks : 0);
+  if (st != RSR_OK) return st;
+  if (!plan) return fail(RSR_ERR_INVALID, "null plan");
+  return batch_plan_build(*desc, plan, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t rsr_multiply_batched_plan_workspace_bytes(const rsr_batch_plan* plan, int64_t batch) {
+  return plan ? batched_plan_workspace_bytes(*plan, batch) : 0;
+}
+
+rsr_status rsr_multiply_batched_plan(const rsr_index_desc* desc, const rsr_batch_plan* plan, const int32_t* V,
+                                     int64_t batch, int32_t* OUT, rsr_variant variant, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+  rsr_status st = check_range(desc, 0, desc ? desc->nblocks : 0);
+  if (st != RSR_OK) return st;
+  if (!plan) return fail(RSR_ERR_INVALID, "null plan");
+  if (batch < 0) return fail(RSR_ERR_INVALID, "batch must be non-negative");
+  if (batch > 0 && (!V || !OUT)) return fail(RSR_ERR_INVALID, "null vector or output");
+  if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
+    return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
+  return multiply_batched_plan(*desc, *plan, V, batch, OUT, variant, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t rsr_multiply_batched_workspace_bytes(const rsr_index_desc* desc, int64_t batch, rsr_dtype v_dtype) {

@@ -395,8 +395,46 @@ def multiply_parallel(v, idx, variant: str = "rsrpp", worker_count: int = 1, *, 
     return out.double().cpu().numpy()
 
 
+def batch_plan(idx):
+    """The index re-cut for the batch-native kernel (rsr_batch_plan_*, csrc/batch_lanes.cu):
+    built on the device on first use (one host synchronisation, never while the stream is
+    being captured) and kept with the index.  None when the batch kernel does not apply."""
+    import torch
+    bp = idx._bplan
+    if bp is None:
+        if torch.cuda.is_current_stream_capturing():
+            return None
+        L = _native.lib()
+        pl = _native.BatchPlan()
+        cb, mb, wb = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        st = L.rsr_batch_plan_layout(ctypes.byref(idx.desc), ctypes.byref(pl), ctypes.byref(cb), ctypes.byref(mb),
+                                     ctypes.byref(wb))
+        if st == _native.RSR_ERR_UNSUPPORTED:
+            idx._bplan = False
+            return None
+        _native.check(st)
+        codes = torch.empty(max(1, cb.value // 2), dtype=torch.int16, device="cuda")
+        maps = torch.empty(max(1, mb.value // 2), dtype=torch.int16, device="cuda")
+        ws = torch.empty(max(1, wb.value), dtype=torch.uint8, device="cuda")
+        pl.codes, pl.slot_bins = codes.data_ptr(), maps.data_ptr()
+        st = L.rsr_batch_plan_build(ctypes.byref(idx.desc), ctypes.byref(pl), ws.data_ptr(), wb.value,
+                                    _native.current_stream_ptr())
+        if st == _native.RSR_ERR_UNSUPPORTED:
+            idx._bplan = False
+            return None
+        _native.check(st)
+        bp = idx._bplan = (pl, codes, maps)
+    return bp or None
+
+
+_PLAN_OFF = __import__("os").environ.get("RSR_B200_BATCH_PLAN", "1") == "0"  # diagnostics: old batch forms
+
+
 def multiply_batched(V, idx, variant: str = "rsrpp"):
-    """V [batch, rows] CUDA tensor -> [batch, cols] of the same dtype.  Index beyond L2: the
+    """V [batch, rows] CUDA tensor -> [batch, cols] of the same dtype.  int32 batches run the
+    batch-native kernel (batch_plan; csrc/batch_lanes.cu: lanes span 64 vectors, conflict-free
+    reductions, no host synchronisation, CUDA-graph capturable once the plan exists).  Otherwise
+    (fp32, fp64, or no plan): index beyond L2: the
     batched gather kernel (csrc/batched.cu: each index byte read once per slice of up to 128
     vectors).  Index L2-resident: scatter launches, int32 two vectors per launch when the
     device guard proves the packing exact (one host sync per call; include/rsr_b200.h).  fp64
@@ -411,6 +449,17 @@ def multiply_batched(V, idx, variant: str = "rsrpp"):
     if code == _native.I64:
         raise ValueError("batched vectors must be int32, float32 or float64")
     out = torch.empty((V.shape[0], idx.cols), dtype=V.dtype, device=V.device)
+    bp = batch_plan(idx) if (code == _native.I32 and not _PLAN_OFF and V.shape[0] > 1) else None
+    if bp is not None:  # int32: the batch-native kernel (lanes span the vectors; no host sync)
+        pl = bp[0]
+        L = _native.lib()
+        nbytes = L.rsr_multiply_batched_plan_workspace_bytes(ctypes.byref(pl), V.shape[0])
+        ws = torch.empty(max(1, nbytes), dtype=torch.uint8, device=V.device)
+        _native.check(L.rsr_multiply_batched_plan(
+            ctypes.byref(idx.desc), ctypes.byref(pl), V.data_ptr(), V.shape[0], out.data_ptr(),
+            _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR, ws.data_ptr(), nbytes,
+            _native.current_stream_ptr()))
+        return out
     nbytes = _native.lib().rsr_multiply_batched_workspace_bytes(ctypes.byref(idx.desc), V.shape[0], code)
     # int64 elements: at least nbytes (allocations are 256-byte aligned)
     # per-call workspace from torch's stream-ordered caching allocator (never shared across streams)

@@ -545,3 +545,40 @@ def test_batched_under_graph_capture(rsr, cuda):
     assert torch.equal(captured, eager)
     ref = V.cpu().numpy().astype(np.int64) @ A.astype(np.int64)
     assert np.array_equal(eager.cpu().numpy().astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("rows,cols,k,batch,vmax", [
+    (300, 77, 5, 3, 100),        # one plan block pass, odd batch
+    (1003, 37, 6, 70, 100),      # two 64-vector slices, ragged rows and last plan block
+    (16384, 600, 11, 64, 100),   # the headline split (16384 rows), split slots in every unit
+    (16384, 601, 11, 64, 300),   # |v| > 127: the int32-lane form (32 vectors per pass)
+    (20000, 515, 12, 7, 100),    # two row splits (atomic output)
+    (4096, 333, 10, 130, 2**31 - 1),  # int32-range values: wraps like every int32 path
+])
+def test_batch_plan_kernel(rsr, cuda, rows, cols, k, batch, vmax):
+    """The batch-native kernel (csrc/batch_lanes.cu: lanes span 64 vectors, re-cut 9-wide plan
+    blocks with split slots) against exact int64 products (mod 2^32) and against the
+    per-vector path, for both variants and binary indexes; the plan is built once and kept."""
+    import torch
+    from paper_2411_06360_b200 import kernels as K
+    rng = np.random.default_rng([rows, cols, k, batch, vmax % 1000])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    V = rng.integers(-vmax, vmax, size=(batch, rows), endpoint=True, dtype=np.int64).astype(np.int32)
+    idx = rsr.preprocess_ternary(torch.from_numpy(A).cuda(), k)
+    wrap = lambda x: ((x + 2**31) % 2**32) - 2**31  # noqa: E731
+    ref = wrap(V.astype(np.int64) @ A.astype(np.int64))
+    dV = torch.from_numpy(V).cuda()
+    for variant in ("rsrpp", "rsr"):
+        got = rsr.multiply_batched(dV, idx, variant).cpu().numpy()
+        assert idx._bplan, "the batch plan applies here"
+        assert np.array_equal(got.astype(np.int64), ref), variant
+    K._PLAN_OFF = True
+    try:
+        old = rsr.multiply_batched(dV, idx).cpu().numpy()
+    finally:
+        K._PLAN_OFF = False
+    assert np.array_equal(old, rsr.multiply_batched(dV, idx).cpu().numpy())
+    B = (A == 1).astype(np.uint8)
+    bidx = rsr.preprocess(rsr.BinaryMatrix.from_dense(B), k)
+    gotb = rsr.multiply_batched(dV, bidx).cpu().numpy()
+    assert np.array_equal(gotb.astype(np.int64), wrap(V.astype(np.int64) @ B.astype(np.int64)))
