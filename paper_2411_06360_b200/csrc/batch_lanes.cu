@@ -229,7 +229,7 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
   int32_t* hist = reinterpret_cast<int32_t*>(smem);  // [NBUF][slots][32]
   uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + (size_t)NBUF * slot_words * 4);
   uint64_t* hfree = hfull + kMaxNbuf;
-  int32_t* part = reinterpret_cast<int32_t*>(hfree + kMaxNbuf);  // [2][kLaneFold][2][kPlanKb][32] fold partials
+  int32_t* fpart = reinterpret_cast<int32_t*>(hfree + kMaxNbuf);  // [2][kLaneFold][2][kPlanKb][32] fold partials
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int b = 0; b < NBUF; ++b) {
@@ -254,21 +254,46 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
     pp = r % npass;
     q = r / npass;
   };
-  // scatter warp w: 8-row groups [w * G / W, (w + 1) * G / W) of the unit's split (G = split_rows / 8)
+  // Work items: full units for the whole rounds of the grid, then the remainder units split by
+  // rows into `S` parts each, so the last round keeps every CTA busy (1821 plan blocks = 911
+  // passes over 148 CTAs would otherwise leave a 7th round on 23 CTAs).  Split items add their
+  // columns atomically (the output is zeroed first).
+  const int G = gridDim.x;
+  const int F = nunits / G, R = nunits - F * G;
+  const int S = (R == 0 || F == 0) ? 1 : min(8, max(1, G / R));
+  const int nitems = F * G + R * S;
+  auto item_of = [&](int i, int& q, int& pp, int& s, int& part, int& nparts) {
+    int u = i;
+    part = 0;
+    nparts = 1;
+    if (i >= F * G) {
+      const int k = i - F * G;
+      u = F * G + k / S;
+      part = k % S;
+      nparts = S;
+    }
+    unit_of(u, q, pp, s);
+  };
+  // scatter warp w of an item: its share of the item's 8-row groups (part `part` of `nparts` of
+  // the split's split_rows / 8 groups)
   const int gsplit = p.split_rows / 8;
-  const int gw0 = warp * gsplit / kLaneWarps, gw1 = (warp + 1) * gsplit / kLaneWarps;
-  const int ng = gw1 - gw0;
-  const int wr = 8 * ng;  // rows of this warp
+  auto warp_groups = [&](int part, int nparts, int& g0, int& n) {
+    const int p0 = part * gsplit / nparts, p1 = (part + 1) * gsplit / nparts;  // the part's groups
+    g0 = p0 + warp * (p1 - p0) / kLaneWarps;
+    n = p0 + (warp + 1) * (p1 - p0) / kLaneWarps - g0;
+  };
 
   if (warp < kLaneWarps) {
     // =============================== scatter warps ===============================
     // transposed histogram: lane w's words of every slot form one row of `slots` words (odd), so
     // the 32 lanes of a reduction hit 32 distinct banks whatever the slot
     const uint32_t hs = smem_u32(hist) + (uint32_t)lane * p.slots * 4u;
-    int t = 0;  // block sequence number of this CTA (2 per unit)
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x, t += 2) {
-      int q, pp, s;
-      unit_of(u, q, pp, s);
+    int t = 0;  // block sequence number of this CTA (2 per item)
+    for (int it = blockIdx.x; it < nitems; it += G, t += 2) {
+      int q, pp, s, part, nparts, gw0, ng;
+      item_of(it, q, pp, s, part, nparts);
+      warp_groups(part, nparts, gw0, ng);
+      const int wr = 8 * ng;  // rows of this warp
       const int bA = 2 * pp;
       const bool hasB = bA + 1 < p.nblocks;
       const int bufA = t % NBUF, bufB = (t + 1) % NBUF;
@@ -278,13 +303,14 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
       const int64_t hstride = (int64_t)p.nblocks * p.row_stride;
       const uint4* vrow = (packed ? p.vp : p.vw) + ((int64_t)s * n4 + r0 / 4) * 32 + lane;
       // L2 prefetch of the next unit's code rows of this warp (the code stream comes from HBM)
-      if (lane == 0 && u + (int)gridDim.x < nunits) {
-        int q2, pp2, s2;
-        unit_of(u + gridDim.x, q2, pp2, s2);
-        const int64_t r02 = (int64_t)q2 * p.split_rows + 8 * (int64_t)gw0;
+      if (lane == 0 && it + G < nitems) {
+        int q2, pp2, s2, part2, nparts2, g02, n2;
+        item_of(it + G, q2, pp2, s2, part2, nparts2);
+        warp_groups(part2, nparts2, g02, n2);
+        const int64_t r02 = (int64_t)q2 * p.split_rows + 8 * (int64_t)g02;
         for (int b = 2 * pp2; b < 2 * pp2 + 2 && b < p.nblocks; ++b)
           for (int h = 0; h < (TERNARY ? 2 : 1); ++h)
-            prefetch_l2_bulk(p.codes + (int64_t)h * hstride + (int64_t)b * p.row_stride + r02, (uint32_t)wr * 2u);
+            prefetch_l2_bulk(p.codes + (int64_t)h * hstride + (int64_t)b * p.row_stride + r02, (uint32_t)n2 * 16u);
       }
       if (t >= NBUF) mbar_wait(&hfree[bufA], (uint32_t)((t / NBUF) - 1) & 1u);
       if (t + 1 >= NBUF) mbar_wait(&hfree[bufB], (uint32_t)(((t + 1) / NBUF) - 1) & 1u);
@@ -360,9 +386,10 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
     // warps' partial columns are summed in a fixed order by fold warp 0
     const int f = warp - kLaneWarps;
     int t = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-      int q, pp, s;
-      unit_of(u, q, pp, s);
+    for (int it = blockIdx.x; it < nitems; it += G) {
+      int q, pp, s, part, nparts;
+      item_of(it, q, pp, s, part, nparts);
+      const bool atomic_out = p.nsplits > 1 || nparts > 1;
       for (int half_pass = 0; half_pass < 2; ++half_pass, ++t) {
         const int b = 2 * pp + half_pass;
         const int buf = t % NBUF;
@@ -442,7 +469,7 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&hfree[buf]);  // my part of the buffer read and zeroed
-        int32_t* pt = part + (t & 1) * (kLaneFold * 2 * kPlanKb * 32);
+        int32_t* pt = fpart + (t & 1) * (kLaneFold * 2 * kPlanKb * 32);
 #pragma unroll
         for (int L = 0; L < kPlanKb; ++L) {
           pt[((f * 2 + 0) * kPlanKb + L) * 32 + lane] = ax[L];
@@ -464,17 +491,17 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
             const int64_t v0 = (int64_t)s * 64 + 2 * lane;
             const int32_t lo = (int32_t)((uint32_t)sx - ((uint32_t)sy << 16));
             if (v0 < p.batch) {
-              if (p.atomic_out) atomicAdd(p.out + v0 * p.cols + col, lo);
+              if (atomic_out) atomicAdd(p.out + v0 * p.cols + col, lo);
               else p.out[v0 * p.cols + col] = lo;
             }
             if (v0 + 1 < p.batch) {
-              if (p.atomic_out) atomicAdd(p.out + (v0 + 1) * p.cols + col, sy);
+              if (atomic_out) atomicAdd(p.out + (v0 + 1) * p.cols + col, sy);
               else p.out[(v0 + 1) * p.cols + col] = sy;
             }
           } else {
             const int64_t v0 = (int64_t)s * 32 + lane;
             if (v0 < p.batch) {
-              if (p.atomic_out) atomicAdd(p.out + v0 * p.cols + col, sx);
+              if (atomic_out) atomicAdd(p.out + v0 * p.cols + col, sx);
               else p.out[v0 * p.cols + col] = sx;
             }
           }
@@ -591,8 +618,8 @@ rsr_status multiply_batched_plan(const rsr_index_desc& d, const rsr_batch_plan& 
   p.nbuf = lanes_smem(p.slots, 3) <= max_smem ? 3 : 2;
   const size_t smem = lanes_smem(p.slots, p.nbuf);
   if (smem > max_smem) return fail(RSR_ERR_UNSUPPORTED, "batched plan multiply: histograms do not fit");
-  if (p.atomic_out && (st = cuda_check(cudaMemsetAsync(out, 0, (size_t)batch * d.cols * 4, s), "memset out")) != RSR_OK)
-    return st;
+  // outputs of row-split items are added atomically: start from zero (4 bytes per result)
+  if ((st = cuda_check(cudaMemsetAsync(out, 0, (size_t)batch * d.cols * 4, s), "memset out")) != RSR_OK) return st;
   const bool pp = var == RSR_VARIANT_RSRPP;
   auto kern = d.halves == 2 ? (pp ? lanes_kernel<true, true> : lanes_kernel<false, true>)
                             : (pp ? lanes_kernel<true, false> : lanes_kernel<false, false>);

@@ -554,6 +554,7 @@ def test_batched_under_graph_capture(rsr, cuda):
     (16384, 601, 11, 64, 300),   # |v| > 127: the int32-lane form (32 vectors per pass)
     (20000, 515, 12, 7, 100),    # two row splits (atomic output)
     (4096, 333, 10, 130, 2**31 - 1),  # int32-range values: wraps like every int32 path
+    (1000, 3096, 9, 64, 100),    # 172 passes on 148 CTAs: remainder passes split 6 ways by rows
 ])
 def test_batch_plan_kernel(rsr, cuda, rows, cols, k, batch, vmax):
     """The batch-native kernel (csrc/batch_lanes.cu: lanes span 64 vectors, re-cut 9-wide plan
