@@ -143,6 +143,17 @@ rsr_status rsr_dense_pack_ternary(const int8_t* A, int64_t lda, int64_t rows, in
 rsr_status rsr_dense_multiply(const uint32_t* d_pos, const uint32_t* d_neg, int64_t rows, int64_t cols,
                               const void* v, rsr_dtype dtype, void* out, void* stream);
 
+/* The same comparator at HBM speed for int8-range activations (the reference's own vectors are
+ * integers in [-100, 100]): 2 bits per entry laid out so that IDP4A does four entries per two
+ * instructions.  rsr_dense_pack_ternary_i8: int8 A -> d_q, rsr_dense_i8_words(rows, cols) u32
+ * ([ceil(rows/16)][cols]; entry (16r + 4t + k, j) = 2-bit field t of byte k: 01 = +1, 11 = -1).
+ * rsr_dense_multiply_i8: out[cols] int32 = v[rows] int8 . A, exact. */
+size_t rsr_dense_i8_words(int64_t rows, int64_t cols);
+rsr_status rsr_dense_pack_ternary_i8(const int8_t* A, int64_t lda, int64_t rows, int64_t cols, uint32_t* d_q,
+                                     int32_t* d_bad_entries, void* stream);
+rsr_status rsr_dense_multiply_i8(const uint32_t* d_q, int64_t rows, int64_t cols, const int8_t* v, int32_t* out,
+                                 void* stream);
+
 /* Batched multiply: V [batch][rows] -> OUT [batch][cols] on the current stream (SURVEY.md
  * §8(d) config 3; the reference has no batch API and runs `multiply_ternary`,
  * kernels.py:196-206, once per vector).  int32 and fp32 need `workspace` of

@@ -29,6 +29,7 @@ EXPORTS = (
     "rsr_host_session_create", "rsr_host_session_destroy", "rsr_host_session_multiply", "rsr_segmented_sum",
     "rsr_block_product", "rsr_naive_multiply_ternary",
     "rsr_dense_plane_words", "rsr_dense_pack_ternary", "rsr_dense_multiply",
+    "rsr_dense_i8_words", "rsr_dense_pack_ternary_i8", "rsr_dense_multiply_i8",
     "rsr_batch_plan_layout", "rsr_batch_plan_build", "rsr_multiply_batched_plan_workspace_bytes",
     "rsr_multiply_batched_plan",
 )
@@ -123,6 +124,12 @@ def lib() -> ctypes.CDLL:
     L.rsr_dense_pack_ternary.restype = st
     L.rsr_dense_multiply.argtypes = [P, P, I64, I64, P, ctypes.c_int, P, P]
     L.rsr_dense_multiply.restype = st
+    L.rsr_dense_i8_words.argtypes = [I64, I64]
+    L.rsr_dense_i8_words.restype = SZ
+    L.rsr_dense_pack_ternary_i8.argtypes = [P, I64, I64, I64, P, P, P]
+    L.rsr_dense_pack_ternary_i8.restype = st
+    L.rsr_dense_multiply_i8.argtypes = [P, I64, I64, P, P, P]
+    L.rsr_dense_multiply_i8.restype = st
     L.rsr_naive_multiply_ternary.argtypes = [P, I64, I64, I64, P, ctypes.c_int, P, P]
     L.rsr_naive_multiply_ternary.restype = st
     L.rsr_batch_plan_layout.argtypes = [ctypes.POINTER(IndexDesc), ctypes.POINTER(BatchPlan), ctypes.POINTER(SZ),

@@ -33,6 +33,11 @@ rsr_status multiply_batched_plan(const rsr_index_desc& d, const rsr_batch_plan& 
 rsr_status multiply_wide(const rsr_index_desc& d, const int64_t* v, uint64_t max_abs, void* out, rsr_dtype ot,
                          rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s);
 size_t dense_plane_words(int64_t rows, int64_t cols);
+size_t dense_i8_words(int64_t rows, int64_t cols);
+rsr_status dense_pack_i8(const int8_t* A, int64_t lda, int64_t rows, int64_t cols, uint32_t* Q, int32_t* bad,
+                         cudaStream_t s);
+rsr_status dense_multiply_i8(const uint32_t* Q, int64_t rows, int64_t cols, const int8_t* v, int32_t* out,
+                             cudaStream_t s);
 rsr_status dense_pack_ternary(const int8_t* A, int64_t lda, int64_t rows, int64_t cols, uint32_t* P, uint32_t* N,
                               int32_t* bad, cudaStream_t s);
 rsr_status dense_multiply(const uint32_t* P, const uint32_t* N, int64_t rows, int64_t cols, const void* v,
@@ -363,6 +368,18 @@ rsr_status rsr_dense_pack_ternary(const int8_t* A, int64_t lda, int64_t rows, in
 rsr_status rsr_dense_multiply(const uint32_t* d_pos, const uint32_t* d_neg, int64_t rows, int64_t cols, const void* v,
                               rsr_dtype dtype, void* out, void* stream) {
   return dense_multiply(d_pos, d_neg, rows, cols, v, dtype, out, (cudaStream_t)stream);
+}
+
+size_t rsr_dense_i8_words(int64_t rows, int64_t cols) { return rows > 0 && cols > 0 ? dense_i8_words(rows, cols) : 0; }
+
+rsr_status rsr_dense_pack_ternary_i8(const int8_t* A, int64_t lda, int64_t rows, int64_t cols, uint32_t* d_q,
+                                     int32_t* d_bad_entries, void* stream) {
+  return dense_pack_i8(A, lda, rows, cols, d_q, d_bad_entries, (cudaStream_t)stream);
+}
+
+rsr_status rsr_dense_multiply_i8(const uint32_t* d_q, int64_t rows, int64_t cols, const int8_t* v, int32_t* out,
+                                 void* stream) {
+  return dense_multiply_i8(d_q, rows, cols, v, out, (cudaStream_t)stream);
 }
 
 rsr_status rsr_naive_multiply_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t lda, const void* v,

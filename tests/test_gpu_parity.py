@@ -583,3 +583,16 @@ def test_batch_plan_kernel(rsr, cuda, rows, cols, k, batch, vmax):
     bidx = rsr.preprocess(rsr.BinaryMatrix.from_dense(B), k)
     gotb = rsr.multiply_batched(dV, bidx).cpu().numpy()
     assert np.array_equal(gotb.astype(np.int64), wrap(V.astype(np.int64) @ B.astype(np.int64)))
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (17, 5), (300, 77), (1000, 513), (4096, 4100)])
+def test_dense_i8_comparator(rsr, cuda, rows, cols):
+    """The IDP4A dense comparator (csrc/dense.cu dense_gemv_i8_kernel, 2-bit fields shifted to
+    the top of their byte) is exact for int8 activations, ragged shapes included."""
+    import torch
+    rng = np.random.default_rng([rows, cols, 8])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    v = rng.integers(-128, 128, size=rows).astype(np.int8)
+    d = rsr.DenseTernary(torch.from_numpy(A).cuda())
+    got = d.multiply_i8(torch.from_numpy(v).cuda()).cpu().numpy()
+    assert np.array_equal(got.astype(np.int64), v.astype(np.int64) @ A.astype(np.int64))
