@@ -42,8 +42,8 @@ clean:
 
 # diagnostic build with per-unit timestamps (tools/trace_scatter.py); not used by the product
 TRACE_LIB := paper_2411_06360_b200/lib/trace/librsr_b200_trace.so
-trace: $(SRC) $(HDR)
+trace: $(SRC) $(HDR) $(CXXOBJ)
 	@mkdir -p $(dir $(TRACE_LIB))
-	$(NVCC) $(NVFLAGS) -DRSR_TRACE -shared -o $(TRACE_LIB) $(SRC) $(CXXSRC) -lcudart
+	$(NVCC) $(NVFLAGS) -DRSR_TRACE -shared -o $(TRACE_LIB) $(SRC) $(CXXOBJ) -lcudart
 
 .PHONY: all oracle clean trace

@@ -231,18 +231,27 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     const int b = p.b_begin + col_cta + u * ncol;
     for (int h = 0; h < HALVES; ++h) prefetch_l2_bulk((h ? key1 : key0) + (int64_t)b * p.row_stride + wr0, wbytes);
   };
-  if (lane == 0 && !is_fold && wbytes)
-    for (int u = 0; u <= S && u < nunits; ++u) prefetch_unit(u);  // before the PDL wait
-  if (t == 0) {
+  // before the PDL wait: the first S + 1 units' keys into L2, one bulk prefetch per lane (a bulk
+  // prefetch costs its issuing thread ~0.15 us, so lane 0 alone spent ~1.2 us here)
+  if (!is_fold && wbytes) {
+    const int u = lane / HALVES, h = lane % HALVES;
+    if (u <= S && u < nunits) {
+      const int b = p.b_begin + col_cta + u * ncol;
+      prefetch_l2_bulk((h ? key1 : key0) + (int64_t)b * p.row_stride + wr0, wbytes);
+    }
+  }
+  if (warp == 0) TRACE(2);
+  if (t == 0) {  // (no fence: the mbarriers are only used by this CTA's threads, never by TMA)
     for (int h = 0; h < NH; ++h) {
       mbar_init(&hfull[h], nwarps);
       mbar_init(&hfree[h], FW);
     }
-    fence_mbar_init();
   }
   for (int i = t; i < hist_words / 4; i += blockDim.x) reinterpret_cast<int4*>(hist)[i] = make_int4(0, 0, 0, 0);
+  if (warp == 0) TRACE(3);
   // v and out may belong to the previous kernel in the stream: wait for it here (PDL)
   if (!p.independent) grid_dependency_wait();
+  if (warp == 0) TRACE(4);
   if (!p.atomic_out)  // a single-split launch owns its output columns
     for (int i = t; i < nunits * p.k; i += blockDim.x) {
       const int b = p.b_begin + col_cta + (i / p.k) * ncol;
@@ -316,6 +325,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         for (int e = 0; e < 8; ++e) vr[8 * g + e] = (int32_t)((uint32_t)vr[8 * g + e] + ((uint32_t)b[e] << 16));
       }
     }
+    if (warp == 0) TRACE(5);
     if constexpr (FX) {  // CTA max |v| -> quantization scale
       uint32_t m = 0;
 #pragma unroll

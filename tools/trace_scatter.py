@@ -37,8 +37,11 @@ t0 = T[:, 0][T[:, 0] > 0].min()
 us = lambda x: (x - t0) / 1e3 if x > 0 else float("nan")
 ends = [us(T[c, 7]) for c in range(148)]
 print(f"kernel span {np.nanmax(ends):.2f} us; CTA end min/median/max {np.nanmin(ends):.2f}/{np.nanmedian(ends):.2f}/{np.nanmax(ends):.2f}")
+starts = sorted(us(T[c, 0]) for c in range(148))
+print("CTA start percentiles (us):", [round(starts[i], 2) for i in (0, 37, 74, 111, 147)])
 for c in (0, 74, 147):
-    print(f"CTA {c}: start {us(T[c,0]):.2f} prologue_end {us(T[c,1]):.2f} end {us(T[c,7]):.2f}")
+    print(f"CTA {c}: start {us(T[c,0]):.2f} prefetch {us(T[c,2]):.2f} zeroed {us(T[c,3]):.2f} waited {us(T[c,4]):.2f} "
+          f"v_issued {us(T[c,5]):.2f} prologue_end {us(T[c,1]):.2f} end {us(T[c,7]):.2f}")
     for u in range(12):
         r = T[c, 8 + u * 8: 16 + u * 8]
         if r[0] == 0 and r[3] == 0: continue
