@@ -166,7 +166,9 @@ struct Publish {
   void* host_out;              // device pointer of the mapped result buffer [cols], 4-byte elements
   uint32_t* counter;           // device, 0 between calls (flagged)
   uint32_t* flag;              // device pointer of the mapped flag word (flagged)
-  uint32_t seq;                // tag / flag value of this call (never 0)
+  uint32_t seq;                // tag / flag value of this call (never 0), unless seq_dev is set:
+  const uint32_t* seq_dev;     // device word holding the call's seq (written by the call's own H2D copy,
+                               // so one captured graph serves every call of a session)
 };
 
 // multiply.cu: one fused multiply over blocks [b0, b1).  With `pub`, a single-split scatter

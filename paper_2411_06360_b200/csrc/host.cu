@@ -51,6 +51,13 @@ struct rsr_host_session {
   void* d_wide = nullptr;   // wide-multiply workspace (whole int64 range), allocated on first use
   size_t wide_bytes = 0;
   uint32_t seq = 0;
+  // Publishing calls (int32 / fp32 scatter) replay a captured graph: H2D of v plus the call's
+  // seq word (staged right after v) -> the publishing multiply, one cudaGraphLaunch instead of a
+  // memcpy and a kernel launch (~4 us of host time); [kind: int32, fp32][variant]
+  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int direct_calls[2][2] = {{0, 0}, {0, 0}};
+  cudaStream_t cap = nullptr;
+  size_t seq_off = 0;       // byte offset of the seq word in h_v / d_v
 };
 
 using rsr::cuda_check;
@@ -68,6 +75,10 @@ void session_free(rsr_host_session* h) {
   if (h->d_v) cudaFree(h->d_v);
   if (h->d_out) cudaFree(h->d_out);
   if (h->d_wide) cudaFree(h->d_wide);
+  for (auto& gk : h->graph)
+    for (auto& g : gk)
+      if (g) cudaGraphExecDestroy(g);
+  if (h->cap) cudaStreamDestroy(h->cap);
   delete h;
 }
 
@@ -182,9 +193,11 @@ rsr_status rsr_host_session_create(const rsr_index_desc* desc, rsr_host_session*
     return fail(RSR_ERR_INVALID, "bad index descriptor");
   auto* h = new rsr_host_session();
   h->desc = *desc;
-  const size_t vb = 8 * (size_t)desc->rows;
+  h->seq_off = (4 * (size_t)desc->rows + 15) & ~(size_t)15;  // after a 4-byte-element v
+  const size_t vb = std::max(8 * (size_t)desc->rows, h->seq_off + 16);
   const size_t ob = 8 * (size_t)desc->cols;
   rsr_status st = cuda_check(cudaHostAlloc(&h->h_v, vb, cudaHostAllocDefault), "session pinned v");
+  if (st == RSR_OK) st = cuda_check(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking), "session capture stream");
   // tagged words up to 8 K columns, the fenced flag beyond (the host reads 8 vs 4 bytes per
   // result against a ~4 us fence + arrival; session_timeline.cu / e2e probes)
   h->tagged = desc->cols <= 8192;
@@ -239,7 +252,11 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, rs
   const rsr_dtype kt = cls.kind == rsr::kStageI32 ? RSR_I32 : cls.kind == rsr::kStageWide ? RSR_I64
                        : cls.kind == rsr::kStageF32 ? RSR_F32 : RSR_F64;  // computed (and staged) type
   const size_t vb = rsr::dsize(kt) * (size_t)d.rows;
-  rsr_status st = cuda_check(cudaMemcpyAsync(h->d_v, h->h_v, vb, cudaMemcpyHostToDevice, s), "H2D v");
+  const bool graph_kind = kt == RSR_I32 || kt == RSR_F32;  // publishing kinds: the H2D is part of the graph
+  rsr_status st = RSR_OK;
+  if (!graph_kind || !h->graph[kt == RSR_I32 ? 0 : 1][variant == RSR_VARIANT_RSRPP ? 1 : 0])
+    st = cuda_check(cudaMemcpyAsync(h->d_v, h->h_v, graph_kind ? h->seq_off + 16 : vb, cudaMemcpyHostToDevice, s),
+                    "H2D v");
   if (st != RSR_OK) return st;
   bool published = false;
   rsr_dtype rt = kt;  // device result type
@@ -257,9 +274,41 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, rs
                             h->wide_bytes, s);
   } else {
     const uint32_t seq = ++h->seq == 0 ? ++h->seq : h->seq;  // never 0 (the buffer's initial tag)
-    const rsr::Publish pub = h->tagged ? rsr::Publish{h->h_tag_dev, nullptr, nullptr, nullptr, seq}
-                                       : rsr::Publish{nullptr, h->h_res_dev, h->d_counter, h->h_flag_dev, seq};
-    st = rsr::multiply(d, h->d_v, kt, h->d_out, kt, variant, RSR_FORM_AUTO, 0, d.nblocks, s, &pub, &published);
+    const int gk = kt == RSR_I32 ? 0 : 1, gv = variant == RSR_VARIANT_RSRPP ? 1 : 0;
+    const uint32_t* seq_dev = reinterpret_cast<const uint32_t*>((char*)h->d_v + h->seq_off);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    // graphs for the 4-byte kinds only (the seq word sits right after a 4-byte-element v)
+    const bool can_graph = graph_kind && cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+    if (graph_kind) *reinterpret_cast<uint32_t*>((char*)h->h_v + h->seq_off) = seq;
+    if (h->graph[gk][gv] == nullptr && can_graph && h->direct_calls[gk][gv] >= 1) {
+      // capture once (after one direct call, which set the kernels' attributes): H2D(v + seq), multiply
+      const rsr::Publish gpub = h->tagged ? rsr::Publish{h->h_tag_dev, nullptr, nullptr, nullptr, 0, seq_dev}
+                                          : rsr::Publish{nullptr, h->h_res_dev, h->d_counter, h->h_flag_dev, 0, seq_dev};
+      cudaGraph_t g = nullptr;
+      bool gpublished = false;
+      rsr_status cst = cuda_check(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal), "session capture");
+      if (cst == RSR_OK) {
+        rsr_status a = cuda_check(cudaMemcpyAsync(h->d_v, h->h_v, h->seq_off + 16, cudaMemcpyHostToDevice, h->cap), "H2D v");
+        if (a == RSR_OK)
+          a = rsr::multiply(d, h->d_v, kt, h->d_out, kt, variant, RSR_FORM_AUTO, 0, d.nblocks, h->cap, &gpub, &gpublished);
+        const cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+        if (a == RSR_OK && e == cudaSuccess && gpublished) {
+          cudaGraphExec_t ex = nullptr;
+          if (cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) h->graph[gk][gv] = ex;
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();  // a failed capture only means no graph: the direct path stays
+      }
+    }
+    if (can_graph && h->graph[gk][gv]) {
+      st = cuda_check(cudaGraphLaunch(h->graph[gk][gv], s), "session graph launch");
+      published = true;
+    } else {
+      if (graph_kind) ++h->direct_calls[gk][gv];
+      const rsr::Publish pub = h->tagged ? rsr::Publish{h->h_tag_dev, nullptr, nullptr, nullptr, seq, nullptr}
+                                         : rsr::Publish{nullptr, h->h_res_dev, h->d_counter, h->h_flag_dev, seq, nullptr};
+      st = rsr::multiply(d, h->d_v, kt, h->d_out, kt, variant, RSR_FORM_AUTO, 0, d.nblocks, s, &pub, &published);
+    }
     if (st == RSR_OK && published) {
       if (tr) { t1 = now_us(); g_trace.v[1].push_back(t1 - t0); t0 = t1; }
       // int32 / int64 vectors staged as int32 deliver int32 results

@@ -25,17 +25,19 @@ constexpr double kTwo63 = 9223372036854775808.0;
 uint64_t uabs64(int64_t x) { return x < 0 ? 0 - (uint64_t)x : (uint64_t)x; }
 
 StageInfo stage_i32(const int32_t* __restrict__ src, int64_t n, void* dst, bool force_i32) {
+  // pass 1: copy and max |v| (3 vector ops per 8 entries); max |v| * n <= 2^31 - 1 bounds the sum
   int32_t* __restrict__ d = static_cast<int32_t*>(dst);
-  int64_t sum = 0;
   uint32_t mx = 0;
   for (int64_t i = 0; i < n; ++i) {
     const int32_t x = src[i];
     d[i] = x;
     const uint32_t a = x < 0 ? 0u - (uint32_t)x : (uint32_t)x;
-    sum += a;
     mx = a > mx ? a : mx;
   }
-  if (force_i32 || sum <= kI32Max) return {kStageI32, mx};
+  if (force_i32 || (uint64_t)mx * (uint64_t)n <= (uint64_t)kI32Max) return {kStageI32, mx};
+  int64_t sum = 0;  // pass 2 (large activations only): the exact bound
+  for (int64_t i = 0; i < n; ++i) sum += src[i] < 0 ? -(int64_t)src[i] : (int64_t)src[i];
+  if (sum <= kI32Max) return {kStageI32, mx};
   int64_t* __restrict__ w = static_cast<int64_t*>(dst);
   for (int64_t i = n - 1; i >= 0; --i) w[i] = src[i];  // widen (src is the caller's buffer)
   return {kStageWide, mx};

@@ -693,7 +693,8 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       __threadfence();  // my output reductions / stores are performed at L2 before the barrier
       asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
       if (fw == 0) TRACE(500);
-      const unsigned long long tag = (unsigned long long)p.pub.seq << 32;
+      const uint32_t seq = p.pub.seq_dev ? *p.pub.seq_dev : p.pub.seq;
+      const unsigned long long tag = (unsigned long long)seq << 32;
       uint32_t* hout = reinterpret_cast<uint32_t*>(p.pub.host_out);
       for (int i = ft; i < nunits * p.k; i += 32 * FW) {
         const int b = p.b_begin + col_cta + (i / p.k) * ncol;
@@ -715,7 +716,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
           if (atomicAdd(p.pub.counter, 1u) == gridDim.x - 1) {
             __threadfence_system();
             *p.pub.counter = 0;  // ready for the next call (stream-ordered)
-            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pub.flag), "r"(p.pub.seq) : "memory");
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pub.flag), "r"(seq) : "memory");
           }
         }
       }
