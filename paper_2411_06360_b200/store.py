@@ -57,13 +57,14 @@ def save_index(idx, path) -> None:
 
 # ----------------------------------------------------------------------------- reading
 def _read_half(raw: bytes, offset: int, rows: int, cols: int, k: int, block_count: int):
-    """Structure checks of store.py:48-77; returns (perm u32 [NB, rows], seg u32 [NB, 2^k], offset)."""
-    expected = column_blocks(cols, k)
+    """Structure checks of store.py:48-66 in the reference's order; returns (per-block perm
+    views, per-block seg views, offset).  No array is allocated before its bytes are known to
+    exist (a corrupt k cannot ask for 2^k entries)."""
+    expected = column_blocks(cols, k)  # ValueError for k < 1, as the reference
     if block_count != len(expected):
         raise FormatError(f"block_count {block_count} does not match ceil(cols/k)")
-    perm = np.empty((len(expected), rows), np.uint32)
-    seg = np.zeros((len(expected), 1 << k), np.uint32)
-    for b, (_, width) in enumerate(expected):
+    perms, segs = [], []
+    for _, width in expected:
         if offset + 2 > len(raw):
             raise FormatError("truncated block header")
         (stored_width,) = struct.unpack_from("<H", raw, offset)
@@ -73,27 +74,41 @@ def _read_half(raw: bytes, offset: int, rows: int, cols: int, k: int, block_coun
         nbytes = 4 * rows + 4 * (1 << width)
         if offset + nbytes > len(raw):
             raise FormatError("truncated payload")
-        perm[b] = np.frombuffer(raw, "<u4", count=rows, offset=offset)
-        seg[b, :1 << width] = np.frombuffer(raw, "<u4", count=1 << width, offset=offset + 4 * rows)
+        perms.append(np.frombuffer(raw, "<u4", count=rows, offset=offset))
+        segs.append(np.frombuffer(raw, "<u4", count=1 << width, offset=offset + 4 * rows))
         offset += nbytes
-    return perm, seg, offset
+    return perms, segs, offset
 
 
-def _block_error(perm: np.ndarray, seg: np.ndarray, rows: int, width: int, b: int) -> str:
-    """The reference's message for failing block b (indexer.py:110-122, same order)."""
+def _block_error(perm: np.ndarray, seg: np.ndarray, rows: int, b: int):
+    """The reference's message for block b, or None (indexer.py:110-122, same order)."""
     p = perm.astype(np.int64)
     counts = np.bincount(np.minimum(p, rows), minlength=rows + 1)[:rows]
     if p.size and (p.max() >= rows or (counts != 1).any()):
         return f"block {b}: permutation is not a bijection"
-    s = seg[:1 << width].astype(np.int64)
+    s = seg.astype(np.int64)
     if s[0] != 0:
         return f"block {b}: segmentation must start at 0"
-    return f"block {b}: segmentation must be non-decreasing and <= rows"
+    if (np.diff(s) < 0).any() or s[-1] > rows:
+        return f"block {b}: segmentation must be non-decreasing and <= rows"
+    return None
+
+
+def _half_violation(perms, segs, rows: int):
+    """First failing block of one half in the reference's order (RsrIndex.from_blocks), or None.
+    Host NumPy, used only on error paths: the device import validates the good case."""
+    for b, (p, s) in enumerate(zip(perms, segs)):
+        msg = _block_error(p, s, rows, b)
+        if msg:
+            return msg
+    return None
 
 
 def load_index(path, device=None):
     """Read and re-validate an index file (store.py:80-101); returns an RsrIndex or a
-    TernaryIndex resident in HBM."""
+    TernaryIndex resident in HBM.  Errors come in the reference's order: the header, then for
+    each half its structure and then its invariants (k, then block by block), then trailing
+    bytes."""
     import torch
     raw = Path(path).read_bytes()
     if len(raw) < HEADER_BYTES:
@@ -107,17 +122,38 @@ def load_index(path, device=None):
         raise FormatError(f"unknown index kind {kind}")
     if rows < 1 or cols < 1:
         raise FormatError("index dimensions must be at least 1x1")
-    try:
-        _check_k(k, rows)
-    except ValueError as exc:
-        raise FormatError(f"invariant violation: {exc}") from None
     offset = HEADER_BYTES
     halves = []
-    for _ in range(2 if kind == _KIND_TERNARY else 1):
-        perm, seg, offset = _read_half(raw, offset, rows, cols, k, block_count)
-        halves.append((perm, seg))
+    for h in range(2 if kind == _KIND_TERNARY else 1):
+        try:
+            perms, segs, offset = _read_half(raw, offset, rows, cols, k, block_count)
+        except FormatError:
+            # the reference validated the previous half before reading this one
+            if halves:
+                msg = _half_violation(*halves[-1], rows)
+                if msg:
+                    raise FormatError(f"invariant violation: {msg}") from None
+            raise
+        try:  # RsrIndex.from_blocks checks k first (indexer.py:96)
+            _check_k(k, rows)
+        except ValueError as exc:
+            raise FormatError(f"invariant violation: {exc}") from None
+        halves.append((perms, segs))
     if offset != len(raw):
+        for hp in halves:
+            msg = _half_violation(*hp, rows)
+            if msg:
+                raise FormatError(f"invariant violation: {msg}")
         raise FormatError("trailing bytes")
+    widths = [w for _, w in column_blocks(cols, k)]
+    stacked = []
+    for perms, segs in halves:
+        perm = np.stack(perms).astype(np.uint32)
+        seg = np.zeros((len(widths), 1 << k), np.uint32)
+        for b, (sg, w) in enumerate(zip(segs, widths)):
+            seg[b, :1 << w] = sg
+        stacked.append((perm, seg))
+    halves = stacked
 
     arrays = _DeviceArrays(rows, cols, k, len(halves), device)
     dev = arrays.device
@@ -132,23 +168,12 @@ def load_index(path, device=None):
         ctypes.byref(arrays.desc), d_in[0][0].data_ptr(), d_in[0][1].data_ptr(),
         p1.data_ptr() if p1 is not None else None, s1.data_ptr() if s1 is not None else None,
         1 << k, ws.data_ptr(), ws.numel() * 4, err.data_ptr(), _native.current_stream_ptr()))
-    flags, bad = (int(x) for x in err.cpu())
-    if flags:
-        widths = [w for _, w in column_blocks(cols, k)]
-        for perm, seg in halves:  # the first half holding the lowest failing block
-            msg_block = None
-            for b in ([bad] if bad < len(widths) else []):
-                ok = True
-                p = perm[b].astype(np.int64)
-                s = seg[b, :1 << widths[b]].astype(np.int64)
-                if (p >= rows).any() or (np.bincount(np.minimum(p, rows), minlength=rows + 1)[:rows] != 1).any():
-                    ok = False
-                elif s[0] != 0 or (np.diff(s) < 0).any() or s[-1] > rows:
-                    ok = False
-                if not ok:
-                    msg_block = _block_error(perm[b], seg[b], rows, widths[b], b)
-            if msg_block:
-                raise FormatError(f"invariant violation: {msg_block}")
+    flags, _ = (int(x) for x in err.cpu())
+    if flags:  # word the error as the reference would: half 0 block by block, then half 1
+        for perm, seg in halves:
+            msg = _half_violation(list(perm), [seg[b, :1 << w] for b, w in enumerate(widths)], rows)
+            if msg:
+                raise FormatError(f"invariant violation: {msg}")
         raise FormatError("invariant violation: index arrays failed validation")
     if kind == _KIND_BINARY:
         return RsrIndex(arrays, 0)

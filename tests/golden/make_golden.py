@@ -158,6 +158,7 @@ def rsx_files() -> dict:
     out["binary_y"] = rsr.multiply_rsr(vb, bidx)
     good = open(os.path.join(rsx_dir, "binary_90x33_k4.rsx"), "rb").read()
     hdr = store.HEADER_BYTES
+    _HEADER_T = struct.Struct("<4sHBQQHI")
     first_perm = hdr + 2                       # block 0: u16 width, then perm u32 [rows]
     first_seg = first_perm + 4 * 90
     def put_u32(raw, off, val):
@@ -178,6 +179,27 @@ def rsx_files() -> dict:
         "seg_start": put_u32(good, first_seg, 1),
         "seg_order": put_u32(good, first_seg + 4 * 3, 0),
     }
+    # ternary files: which half / block / check the reference names first (store.py:80-101
+    # validates each half completely before reading the next; k is checked by from_blocks)
+    tgood = open(os.path.join(rsx_dir, "ternary_200x77_k5.rsx"), "rb").read()
+    nb5 = -(-77 // 5)
+    half_bytes = sum(2 + 4 * 200 + 4 * (1 << min(5, 77 - 5 * b)) for b in range(nb5))
+    def tblock(h, b):  # byte offset of block b of half h (its u16 width)
+        return hdr + h * half_bytes + sum(2 + 4 * 200 + 4 * (1 << min(5, 77 - 5 * c)) for c in range(b))
+    def dup_perm(raw, h, b):  # perm[1] := perm[0] in block b of half h
+        off = tblock(h, b) + 2
+        return put_u32(raw, off + 4, struct.unpack_from("<I", raw, off)[0])
+    corrupt.update({
+        "t_pos5_neg2": dup_perm(dup_perm(tgood, 0, 5), 1, 2),     # both halves bad: positive block 5 first
+        "t_neg3": dup_perm(tgood, 1, 3),                             # only the negative half
+        "t_pos1_truncneg": dup_perm(tgood, 0, 1)[:tblock(1, 4)],     # positive invariant vs negative truncation
+        "t_pos4_trailing": dup_perm(tgood, 0, 4) + b"\x00",         # positive invariant vs trailing bytes
+        "t_k_exceeds": tgood[:23] + struct.pack("<H", 9) + tgood[25:],  # k = 9: block count no longer matches
+        "t_k_zero": tgood[:23] + struct.pack("<H", 0) + tgood[25:],
+        # a well-formed binary file whose k exceeds floor(log2 rows) (from_blocks' _check_k)
+        "k_exceeds_rows": (_HEADER_T.pack(b"RSX1", 1, 1, 200, 8, 8, 1) + struct.pack("<H", 8)
+                           + np.arange(200, dtype="<u4").tobytes() + np.zeros(256, "<u4").tobytes()),
+    })
     verdicts = {}
     for name, raw in corrupt.items():
         path = os.path.join(rsx_dir, f"corrupt_{name}.rsx")
@@ -187,6 +209,8 @@ def rsx_files() -> dict:
             verdicts[name] = None
         except rsr.FormatError as exc:
             verdicts[name] = str(exc)
+        except ValueError as exc:  # not a FormatError (e.g. column_blocks on k = 0)
+            verdicts[name] = "ValueError: " + str(exc)
     json.dump(verdicts, open(os.path.join(rsx_dir, "verdicts.json"), "w"), indent=1, sort_keys=True)
     return out
 

@@ -334,7 +334,7 @@ def test_rsx_load_golden(rsr, cuda):
     got = rsr.multiply_ternary(torch.from_numpy(prods["ternary_v"].astype(np.int32)).cuda(), tidx)
     assert np.array_equal(got.cpu().numpy().astype(np.float64), prods["ternary_y"])
     verdicts = json.load(open(os.path.join(rsx, "verdicts.json")))
-    for name in ("perm_duplicate", "perm_range", "seg_start", "seg_order"):
+    for name in ("perm_duplicate", "perm_range", "seg_start", "seg_order", "t_pos5_neg2", "t_neg3"):
         with pytest.raises(rsr.FormatError) as exc:
             rsr.load_index(os.path.join(rsx, f"corrupt_{name}.rsx"))
         assert str(exc.value) == verdicts[name], name
