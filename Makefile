@@ -15,7 +15,9 @@ CXXFLAGS_HOST := -O3 -march=x86-64-v3 -fPIC -std=c++17 -Wall -Wextra
 PYINC := $(shell python3 -c "import sysconfig; print(sysconfig.get_paths()['include'])")
 PYEXT := paper_2411_06360_b200/lib/_rsrhost$(shell python3 -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
 
-all: $(LIB) $(PYEXT) oracle
+COUNT_LIB := paper_2411_06360_b200/lib/count/librsr_b200_count.so
+
+all: $(LIB) $(PYEXT) $(COUNT_LIB) oracle
 
 # CPython binding of the host-buffer session (links the library through $ORIGIN)
 $(PYEXT): paper_2411_06360_b200/csrc/pyhost.c include/rsr_b200.h $(LIB)
@@ -37,7 +39,7 @@ oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build $(LIB) $(PYEXT)
+	rm -rf build $(LIB) $(PYEXT) $(COUNT_LIB)
 	$(MAKE) -s -C oracle clean
 
 # diagnostic build with per-unit timestamps (tools/trace_scatter.py); not used by the product
@@ -46,4 +48,14 @@ trace: $(SRC) $(HDR) $(CXXOBJ)
 	@mkdir -p $(dir $(TRACE_LIB))
 	$(NVCC) $(NVFLAGS) -DRSR_TRACE -shared -o $(TRACE_LIB) $(SRC) $(CXXOBJ) -lcudart
 
-.PHONY: all oracle clean trace
+# work-count build: the scatter kernel counts the accumulate steps it executes
+# (rsr_debug_count_copy); used by tests/test_counted_gpu.py, never by the product
+$(OBJDIR)/multiply_count.o: paper_2411_06360_b200/csrc/multiply.cu $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -DRSR_COUNT -c $< -o $@
+$(COUNT_LIB): $(filter-out $(OBJDIR)/multiply.o,$(OBJ)) $(OBJDIR)/multiply_count.o $(CXXOBJ)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -Xlinker -soname=librsr_b200_count.so -o $@ $^ -lcudart
+count: $(COUNT_LIB)
+
+.PHONY: all oracle clean trace count

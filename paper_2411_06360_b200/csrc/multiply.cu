@@ -100,6 +100,30 @@ namespace {
 #define TRACE(slot) do { } while (0)
 #endif
 
+// Work-count build only (`make count`, -DRSR_COUNT, the reference's counted twins
+// kernels.py:240-320): every thread counts the accumulate steps it actually executes —
+// [0] histogram reductions (one per row, half and block: the reference's segmented-sum adds),
+// [1] fold adds (pairwise compaction, chunk and slot accumulation, output atomics),
+// [2] lane adds inside warp reductions (31 per REDUX) — and adds them to g_count at exit.
+#ifdef RSR_COUNT
+__device__ unsigned long long g_count[4];
+#define CNT(var, n) ((var) += (unsigned long long)(n))
+}  // namespace
+}  // namespace rsr
+extern "C" int rsr_debug_count_copy(unsigned long long* host, int reset) {
+  int e = (int)cudaMemcpyFromSymbol(host, rsr::g_count, sizeof(rsr::g_count));
+  if (!e && reset) {
+    static const unsigned long long z[4] = {0, 0, 0, 0};
+    e = (int)cudaMemcpyToSymbol(rsr::g_count, z, sizeof(z));
+  }
+  return e;
+}
+namespace rsr {
+namespace {
+#else
+#define CNT(var, n) ((void)0)
+#endif
+
 struct ScatterParams {
   const uint16_t* key[2];
   const int32_t* v;
@@ -222,6 +246,8 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   OutT* out2 = reinterpret_cast<OutT*>(p.out2);
   const bool is_fold = warp >= nwarps;
   if (warp == 0) TRACE(0);
+  unsigned long long cnt_red = 0, cnt_fold = 0, cnt_redux = 0;  // work counts (RSR_COUNT builds only)
+  (void)cnt_red; (void)cnt_fold; (void)cnt_redux;
 
   // ---- prologue (index only: may overlap the previous kernel under PDL) ----
   const int64_t wr0 = r0 + (int64_t)warp * WROWS;  // first row of this (scatter) warp
@@ -356,6 +382,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         const uint32_t c1 = CODES == 2 ? (w4[e] >> 16) << 2 : w4[e] >> 16;
         // SKIP0: predicated inside the asm (an `if` around it would branch per reduction)
         auto red = [&](uint32_t a, int32_t val, int32_t x) {
+          CNT(cnt_red, SKIP0 ? (x != 0) : 1);
           if constexpr (SKIP0) red_add_shared_if(a, val, x != 0);
           else red_add_shared(a, val);
         };
@@ -377,7 +404,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
         uint4& q0g = q0[g % KA];
-        uint4& q1g = q1[g % KA];
+        [[maybe_unused]] uint4& q1g = q1[g % KA];
         // slot s of the group holds row p[s], p = butterfly of the control bits (k <= 11):
         // route the v registers the same way, once for both halves
         int32_t vp[8];
@@ -479,8 +506,10 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
                   if (tt < cnt) {
                     odd += x[2 * tt + 1];
                     x[tt] = x[2 * tt] + x[2 * tt + 1];
+                    CNT(cnt_fold, 2);
                   }
                 a[L] += odd;
+                CNT(cnt_fold, 1);
               }
               tot = x[0];
             } else {
@@ -489,6 +518,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 #pragma unroll
                 for (int L = 0; L < 4; ++L) a[L] += ((e >> L) & 1) ? x[e] : 0;
                 tot += x[e];
+                CNT(cnt_fold, 1 + __popc(e & 15));
               }
             }
             // chunk bits 4.. (chunk index c4/4) are local bits too
@@ -496,6 +526,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
 #pragma unroll
             for (int L = 4; L < 8; ++L) a[L] += ((ci >> (L - 4)) & 1) ? tot : 0;
             X += tot;
+            CNT(cnt_fold, 1 + __popc(ci & 15));
           }
         } else {
 #pragma unroll
@@ -504,6 +535,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
               const int32_t x = H[key_swizzle((uint32_t)(fbase + e))];
               if (lb >= 1 && (e & 1)) a[0] += x;
               X += x;
+              CNT(cnt_fold, 1 + (lb >= 1 && (e & 1)));
             }
         }
       }
@@ -513,13 +545,16 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         if (i < lb) {
           const int32_t tv = __reduce_add_sync(0xffffffffu, a[i]);
           if (lane == i) r = tv;
+          CNT(cnt_redux, lane == 0 ? 31 : 0);
         }
 #pragma unroll
       for (int bit = 0; bit < 5; ++bit) {
         const int32_t tv = __reduce_add_sync(0xffffffffu, ((lane >> bit) & 1) ? X : 0);
         if (lane == 8 + bit) r = tv;
+        CNT(cnt_redux, lane == 0 ? 31 : 0);
       }
       const int32_t W = __reduce_add_sync(0xffffffffu, X);
+      CNT(cnt_redux, lane == 0 && FB > 0 ? 31 : 0);
 #pragma unroll
       for (int fb2 = 0; fb2 < FB; ++fb2)
         if (lane == 13 + fb2) r = ((fw >> fb2) & 1) ? W : 0;
@@ -679,6 +714,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         }
       } else {
         if (sh >= 0 && sh < w && d[0] != 0) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)d[0]);
+        CNT(cnt_fold, sh >= 0 && sh < w && d[0] != 0);
         if constexpr (PACK)
           if (sh >= 0 && sh < w && d[OLIMBS - 1] != 0) atomicAdd(out2 + (int64_t)b * p.k + (w - 1 - sh), (OutT)d[OLIMBS - 1]);
       }
@@ -723,6 +759,11 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     }
   }
   if (warp == 0) TRACE(7);
+#ifdef RSR_COUNT
+  if (cnt_red) atomicAdd(&g_count[0], cnt_red);
+  if (cnt_fold) atomicAdd(&g_count[1], cnt_fold);
+  if (cnt_redux) atomicAdd(&g_count[2], cnt_redux);
+#endif
 }
 
 // =====================================================================================
@@ -740,7 +781,6 @@ struct GatherParams {
 };
 
 constexpr int kGatherWarps = 8;
-constexpr int kPermAhead = 4;  // perm windows in flight per warp (16-byte loads, registers)
 constexpr int kMaxWin = 64;    // window-end records buffered per warp (expanded when full)
 
 template <typename T>
@@ -1236,6 +1276,7 @@ rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* 
     case RSR_I32: return multiply_gather_t<int32_t>(d, v, out, pp, b0, b1, s);
     case RSR_F32: return multiply_gather_t<float>(d, v, out, pp, b0, b1, s);
     case RSR_F64: return multiply_gather_t<double>(d, v, out, pp, b0, b1, s);
+    default: break;
   }
   return fail(RSR_ERR_INVALID, "unknown dtype");
 }
@@ -1309,6 +1350,7 @@ rsr_status segmented_sum(const rsr_index_desc& d, int half, int block, const voi
     case RSR_I32: segmented_sum_kernel<int32_t><<<grid, 256, 0, s>>>(perm, d.perm_bytes, seg, (const int32_t*)v, nbk, (int32_t*)u); break;
     case RSR_F32: segmented_sum_kernel<float><<<grid, 256, 0, s>>>(perm, d.perm_bytes, seg, (const float*)v, nbk, (float*)u); break;
     case RSR_F64: segmented_sum_kernel<double><<<grid, 256, 0, s>>>(perm, d.perm_bytes, seg, (const double*)v, nbk, (double*)u); break;
+    default: return fail(RSR_ERR_INVALID, "segmented sum takes int32, float32 or float64");
   }
   return cuda_check(cudaGetLastError(), "segmented_sum_kernel launch");
 }
@@ -1325,6 +1367,7 @@ rsr_status naive_ternary(const int8_t* A, int64_t rows, int64_t cols, int64_t ld
     case RSR_I32: naive_ternary_kernel<int32_t><<<grid, 256, 0, s>>>(A, rows, cols, lda, (const int32_t*)v, (int32_t*)out); break;
     case RSR_F32: naive_ternary_kernel<float><<<grid, 256, 0, s>>>(A, rows, cols, lda, (const float*)v, (float*)out); break;
     case RSR_F64: naive_ternary_kernel<double><<<grid, 256, 0, s>>>(A, rows, cols, lda, (const double*)v, (double*)out); break;
+    default: return fail(RSR_ERR_INVALID, "naive multiply takes int32, float32 or float64");
   }
   return cuda_check(cudaGetLastError(), "naive_ternary_kernel launch");
 }
