@@ -288,7 +288,9 @@ def _config_key(args, cfg, k):
     return {"workload": desc, "n": n, "m": m, "k": k, "batch": BATCH.get(args.config, 1)}
 
 
-def run_ours(args, cfg):
+def run_ours(args, cfg, dist=None, lite=False):
+    """One measurement of `cfg`; returns the JSON line (dict).  lite: device timing only (no
+    e2e, comparator or CPU legs) — the nested config-5 measurement of multi-GPU runs."""
     import torch
     import paper_2411_06360_b200 as rsr
     from paper_2411_06360_b200 import _native
@@ -297,11 +299,6 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     domain, n, m, desc = cfg
     # block width: the reference tuner (optimal_k_rsrpp) unless it differs from the measured B200
     # tuner (indexer.optimal_k_b200); results do not depend on k (integer products are exact)
@@ -340,7 +337,7 @@ def run_ours(args, cfg):
     preprocess_s = time.perf_counter() - t0
 
     # ---- the standard dense multiply on the GPU (csrc/dense.cu): comparator
-    dense = rsr.DenseTernary(dA) if domain == "ternary" and not strong else None
+    dense = rsr.DenseTernary(dA) if domain == "ternary" and not strong and not lite else None
 
     # ---- parity gate at full size (untimed): GPU keys + product vs the C oracle
     from oracle import c_oracle
@@ -403,12 +400,13 @@ def run_ours(args, cfg):
     comm = torch.cuda.Stream() if world > 1 else None
     peak, peak_kind = _peaks()
 
-    def capture(var, with_comm):
+    def capture(var, mode):
         """K steps in one CUDA graph.  Step i multiplies index copy i % C into slice buffer
-        i % 2; with_comm: the slice is all-gathered on the comm stream, which overlaps the next
-        step's multiply (the multiply two steps later waits for that gather before reusing the
-        buffer)."""
+        i % 2; mode "overlap": the slice is all-gathered on the comm stream, which overlaps the
+        next step's multiply (the multiply two steps later waits for that gather before reusing
+        the buffer); "serial": the all-gather follows each multiply on the same stream; "none"."""
         fold = var != "rsr"
+        with_comm = mode == "overlap"
         g = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
@@ -422,6 +420,8 @@ def run_ours(args, cfg):
                     if done[b] is not None:
                         cap.wait_event(done[b])
                     K._multiply_device(dv, copies[i % ncopies], fold, None, outs[b][:m])
+                    if mode == "serial":
+                        dist.all_gather_into_tensor(gathered[b], outs[b])
                     if with_comm:
                         ev = torch.cuda.Event()
                         ev.record(cap)
@@ -481,9 +481,25 @@ def run_ours(args, cfg):
             K._multiply_device(dv, copies[i % ncopies], var != "rsr", None, outs[0][:m])
     torch.cuda.synchronize()
 
+    if world > 1:  # communicator warm-up on both streams (NCCL initialises lazily, never inside a capture)
+        dist.all_gather_into_tensor(gathered[0], outs[0])
+        with torch.cuda.stream(comm):
+            dist.all_gather_into_tensor(gathered[1], outs[1])
+        torch.cuda.synchronize()
     results = {}
+    comm_mode, comm_error = ("overlap" if world > 1 else "none"), None
     for var in variants:
-        g = capture(var, world > 1)
+        g = None
+        for mode in ([comm_mode, "serial"] if world > 1 else ["none"]):
+            try:
+                g = capture(var, mode)
+                comm_mode = mode
+                break
+            except Exception as e:  # pragma: no cover - capture of the comm stream refused: serialise
+                comm_error = repr(e)[:200]
+                torch.cuda.synchronize()
+        if g is None:
+            raise SystemExit(f"graph capture failed: {comm_error}")
         med, ms, cs = timed(g)
         results[var] = (med, ms, cs)
         del g
@@ -496,7 +512,7 @@ def run_ours(args, cfg):
     multi = None
     if world > 1:
         # compute-only (no all-gather) and the check of the gathered vector
-        g = capture(variants[0], False)
+        g = capture(variants[0], "none")
         cmed, _, _ = timed(g)
         del g
         kernel_us = cmed / args.steps * 1e3
@@ -515,8 +531,10 @@ def run_ours(args, cfg):
             raise SystemExit("parity failure: the all-gathered vector differs from the ranks' oracle slices")
         multi = {"compute_only_us": cmed / args.steps * 1e3, "with_allgather_us": ms_per_step * 1e3,
                  "allgather_exposed_us": ms_per_step * 1e3 - cmed / args.steps * 1e3,
-                 "allgather_bytes": world * pad * 4, "overlap": "all-gather of step i on a comm stream "
-                 "overlaps the multiply of step i+1 (double-buffered slices)",
+                 "allgather_bytes": world * pad * 4,
+                 "overlap": ("all-gather of step i on a comm stream overlaps the multiply of step i+1 "
+                             "(double-buffered slices)") if comm_mode == "overlap" else
+                            f"serialised all-gather after each multiply ({comm_error})",
                  "gathered_vector_check": "bitwise equal (int32) to the all-gathered per-rank C-oracle slices"
                  if not fp32 else "within 1e-5 norm-wise of the all-gathered per-rank C-oracle slices"}
 
@@ -541,12 +559,14 @@ def run_ours(args, cfg):
             t = float(tt.item())
         return t
 
-    e2e_steps = min(max(args.steps, 20), 500)
+    e2e_steps = 0 if lite else min(max(args.steps, 20), 500)
     scale = 1 if strong else world
     # mapped result words the host reads (csrc/host.cu): 8-byte seq-tagged words up to 8 K
     # columns, 4-byte results behind the fenced flag beyond
     d2h = (8 if m <= 8192 else 4) * m
-    if fp32:
+    if lite:
+        e2e, extra_e2e = None, {}
+    elif fp32:
         e2e_main_ms = e2e_time(v.copy(), e2e_steps)
         e2e = {"value": scale * 1e3 / e2e_main_ms, "unit": "vectors/s", "h2d_bytes_per_step": 4 * n,
                "d2h_bytes_per_step": d2h, "path": "rsr.multiply_ternary(numpy float32 v, idx)"}
@@ -650,15 +670,13 @@ def run_ours(args, cfg):
         line["multi_gpu"] = multi
     if gpu_standard is not None:
         line["gpu_standard"] = gpu_standard
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not lite:
         line["cpu_baseline"] = cpu_baseline(A, v, k_ref, domain, variants[0], args.cpu_seconds)
         if len(variants) > 1:
             line["cpu_baseline_rsr"] = cpu_baseline(A, v, k_ref, domain, "rsr", args.cpu_seconds / 2)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    if lite:
+        line.pop("e2e", None)
+    return line
 
 
 def run_batch(args, cfg, idx, A, v, kp, kn, k, k_ref, preprocess_s, world, rank, dist):
@@ -794,8 +812,7 @@ def run_batch(args, cfg, idx, A, v, kp, kn, k, k_ref, preprocess_s, world, rank,
         line["gpu_standard"] = {"unavailable": str(e)[:200]}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(A, v, k_ref, domain, "rsrpp", args.cpu_seconds, batch=B)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    return line
 
 
 def _count_launches(fn) -> int:
@@ -822,13 +839,40 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--k", type=int, default=0, help="block width override (default: indexer.optimal_k_b200)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-strong", action="store_true", help="N > 1: skip the nested config-5 strong-scaling run")
     args = ap.parse_args()
     args.replays = max(1, args.replays)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
-    else:
-        run_ours(args, cfg)
+        return
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = run_ours(args, cfg, dist)
+    if world > 1 and args.config not in STRONG and not args.no_strong:
+        # BASELINE config 5 beside the default weak-scaling line: ONE 65536^2 matrix column-sharded
+        # over the ranks + all-gather (strong scaling), device timing only
+        import copy
+        a5 = copy.copy(args)
+        a5.config, a5.steps, a5.variant = "ternary65536s", min(args.steps, 50), "rsrpp"
+        try:
+            l5 = run_ours(a5, CONFIGS["ternary65536s"], dist, lite=True)
+            line["config5_strong"] = {key: l5.get(key) for key in
+                                      ("value", "unit", "ms_per_step", "scaling", "config", "notes", "multi_gpu", "roofline")}
+        except (Exception, SystemExit) as e:  # pragma: no cover - the main line stands on its own
+            line["config5_strong"] = {"error": repr(e)[:300]}
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
