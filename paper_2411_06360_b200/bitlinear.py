@@ -4,8 +4,8 @@ A fixed ternary weight matrix W [in_features, out_features] (the reference's v Â
 orientation: activations are row vectors) is preprocessed once into a device index; every
 forward is one `multiply_ternary` (or `multiply_batched` for [B, in] inputs) on the current
 stream, and a chain of layers can be captured in one CUDA graph (single vectors never sync;
-an eager int32 [B, in] call syncs once for the packed-pair guard, and under capture it runs
-one launch per vector instead, include/rsr_b200.h).  An optional
+int32 [B, in] batches run the batch-native kernel, which never syncs once its batch plan â€”
+built on the first batched call â€” exists, include/rsr_b200.h).  An optional
 per-output scale (BitNet's absmean weight scale) is applied after the integer/fixed-point
 product.
 """

@@ -596,3 +596,42 @@ def test_dense_i8_comparator(rsr, cuda, rows, cols):
     d = rsr.DenseTernary(torch.from_numpy(A).cuda())
     got = d.multiply_i8(torch.from_numpy(v).cuda()).cpu().numpy()
     assert np.array_equal(got.astype(np.int64), v.astype(np.int64) @ A.astype(np.int64))
+
+
+def test_seeded_fuzz_every_entry_point(rsr, cuda):
+    """40 seeded random shapes (rows 1..2500, cols 1..1500, every admissible k up to the device
+    limit, ternary and binary) through every public entry point — host int32 / int64 / fp64-integer
+    vectors (session: int32 kernel or wide multiply), device int32 / int64 tensors, block-range
+    multiply_parallel, the batch kernel — each bitwise against the C oracle's exact products."""
+    import torch
+    rng = np.random.default_rng(20241106)
+    for case in range(40):
+        rows = int(rng.integers(1, 2501))
+        cols = int(rng.integers(1, 1501))
+        k = int(rng.integers(1, min(16, rsr.max_k_for_rows(rows)) + 1))
+        ternary = bool(case % 4 != 3)
+        A = rng.integers(-1 if ternary else 0, 2, size=(rows, cols), dtype=np.int8)
+        big = case % 5 == 0  # sums beyond int32: the exact wide multiply
+        v = rng.integers(-(2 ** 30) if big else -100, (2 ** 30) if big else 101, size=rows, dtype=np.int64)
+        M = A.astype(object) if big else A.astype(np.int64)
+        exact = np.array([int(x) for x in (v.astype(object) @ M)] if big else v @ M, dtype=object if big else np.int64)
+        ref = np.array([float(x) for x in exact])
+        if ternary:
+            idx = rsr.preprocess_ternary(torch.from_numpy(A).cuda(), k)
+            mult = rsr.multiply_ternary
+        else:
+            idx = rsr.preprocess(rsr.BinaryMatrix.from_dense(A.astype(np.uint8)), k)
+            mult = rsr.multiply_rsr
+        forms = [v, v.astype(np.float64)] + ([] if big else [v.astype(np.int32)])
+        for form in forms:
+            assert np.array_equal(mult(form, idx), ref), (case, rows, cols, k, form.dtype)
+        assert np.array_equal(rsr.multiply_parallel(v, idx, "rsrpp", int(rng.integers(1, 6))), ref), case
+        dev64 = mult(torch.from_numpy(v).cuda(), idx).cpu().numpy()
+        assert [int(x) for x in dev64] == [int(x) for x in exact], case
+        if not big:
+            dev32 = mult(torch.from_numpy(v.astype(np.int32)).cuda(), idx, "rsr").cpu().numpy()
+            assert np.array_equal(dev32.astype(np.int64), exact), case
+            B = int(rng.integers(2, 70))
+            V = rng.integers(-100, 101, size=(B, rows)).astype(np.int32)
+            got = rsr.multiply_batched(torch.from_numpy(V).cuda(), idx).cpu().numpy()
+            assert np.array_equal(got.astype(np.int64), V.astype(np.int64) @ A.astype(np.int64)), case
