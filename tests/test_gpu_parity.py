@@ -635,3 +635,21 @@ def test_seeded_fuzz_every_entry_point(rsr, cuda):
             V = rng.integers(-100, 101, size=(B, rows)).astype(np.int32)
             got = rsr.multiply_batched(torch.from_numpy(V).cuda(), idx).cpu().numpy()
             assert np.array_equal(got.astype(np.int64), V.astype(np.int64) @ A.astype(np.int64)), case
+
+
+def test_fused_bitlinear_matches_separate_layers(rsr, cuda):
+    """FusedBitLinear (one index over [W_gate | W_up], blocks straddling the two layers) gives each
+    layer's output bitwise equal to the separate BitLinear, single vectors and batches."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(11)
+    Wg = (torch.randint(0, 3, (1024, 1500), device="cuda", dtype=torch.int8, generator=g) - 1).to(torch.int8)
+    Wu = (torch.randint(0, 3, (1024, 1333), device="cuda", dtype=torch.int8, generator=g) - 1).to(torch.int8)
+    fused = rsr.FusedBitLinear([Wg, Wu])
+    sep = [rsr.BitLinear(Wg), rsr.BitLinear(Wu)]
+    x = torch.randint(-100, 101, (1024,), device="cuda", generator=g).to(torch.int32)
+    X = torch.randint(-100, 101, (9, 1024), device="cuda", generator=g).to(torch.int32)
+    for inp in (x, X):
+        for a, b in zip(fused(inp), (s(inp) for s in sep)):
+            assert torch.equal(a, b)
+    with pytest.raises(ValueError):
+        rsr.FusedBitLinear([Wg, Wu[:1000]])

@@ -6,4 +6,4 @@ d=build/alt/$name; mkdir -p $d; rm -f $d/*.o
 for f in paper_2411_06360_b200/csrc/*.cu; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" -c $f -o $d/$(basename ${f%.cu}).o 2>/dev/null &
 done; wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xlinker -soname=librsr_b200.so -o $d/librsr_b200.so $d/*.o -lcudart && echo $d/librsr_b200.so
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xlinker -soname=librsr_b200.so -o $d/librsr_b200.so $d/*.o build/obj/*.cpp.o -lcudart && echo $d/librsr_b200.so
