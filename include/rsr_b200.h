@@ -241,15 +241,16 @@ rsr_status rsr_multiply_host(const rsr_index_desc* desc, const void* v_host, rsr
                              void* d_v, void* d_out, void* stream);
 
 /* Host-buffer session (the e2e call `multiply_ternary(numpy v, idx)`, kernels.py:185-206):
- * pinned staging, device copies of v and of the result, and mapped pinned result memory,
+ * mapped pinned staging, device copies of v and of the result, and mapped pinned result memory,
  * allocated once for one index on the current device.  rsr_host_session_multiply takes v_host
  * [rows] of any element type, v_bytes = its size, and writes out_host [cols] (out_bytes = its size)
  * as float64 (the reference's result type) or as the vector type.  Staging classifies v in the
  * same pass that copies it (csrc/host_stage.cpp), so the result is exact wherever the
  * reference's fp64 result is:
  *   - integer-valued v (int32 / int64, or float64 holding integers) with sum |v| <= 2^31 - 1:
- *     int32 scatter multiply (bit-exact); the launch stores its results straight into the
- *     mapped buffer (no D2H copy, no stream synchronize);
+ *     int32 scatter multiply (bit-exact); with rows <= 16384 the call is ONE kernel launch that
+ *     pulls v from the mapped staging itself and streams each folded block's results into the
+ *     mapped buffer as seq-tagged words (no H2D / D2H copy, no stream synchronize);
  *   - other integer-valued v (|v| < 2^63): the exact wide multiply above;
  *   - float32: fp32 (exact fixed-point scatter while rows <= 16384, else the gather kernel);
  *   - other float64: the fp64 gather kernel.

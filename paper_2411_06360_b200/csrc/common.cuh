@@ -152,24 +152,31 @@ __host__ __device__ __forceinline__ int block_width(int64_t cols, int k, int b) 
   return rem < k ? (int)rem : k;
 }
 
-// Result publishing for host-buffer sessions (csrc/host.cu): a single-split scatter multiply
-// also delivers its results into MAPPED host memory, in one of two ways
-// (tools/microbench/session_timeline.cu measured both):
-//  * tagged (tagged != nullptr): each result is one 64-bit store (seq << 32 | value), single-copy
-//    atomic, and the host accepts a word once its tag is the call's seq.  No fence, counter or
-//    flag, but the host reads 8 bytes per result: the faster scheme up to ~8 K columns.
-//  * flagged (host_out != nullptr): each CTA stores its 4-byte results, one thread releases them
-//    at gpu scope and arrives on a device counter, and the last arrival fences at system scope
-//    (~3 us) and raises the flag the host polls.  4 bytes per result on the host side.
+// Host-buffer sessions (csrc/host.cu): a single-split scatter multiply can take its vector from
+// MAPPED host memory and deliver its results into mapped host memory itself, so one call is one
+// kernel launch (tools/microbench/launch_latency.cu: a graph of one kernel node reaches the GPU
+// in ~4.8 us, one with an H2D copy node ahead of it in ~17 us).
+//  * pull (pull != nullptr): the staged payload (v, 4-byte elements, then the call's seq word at
+//    byte seq_off) is copied by the kernel into `v` (device): CTA c copies chunk c and adds 1 to a
+//    64-bit arrival counter at `sync`; every CTA waits until the counter reaches the end of its
+//    launch's generation (each launch adds exactly grid: one counter per launch shape, never
+//    reset) and, after 20 us, copies the payload itself (copies are identical): no co-residency
+//    is assumed (a grid barrier could deadlock against a concurrent kernel holding SMs).
+//  * tagged results: as soon as a block is folded, each of its columns is written to host memory
+//    as one 64-bit store (seq << 32 | value, single-copy atomic); the host accepts a word once its
+//    tag is the call's seq, so it converts results while later blocks are still running.
 struct Publish {
   unsigned long long* tagged;  // device pointer of the mapped tagged-result buffer [cols]
-  void* host_out;              // device pointer of the mapped result buffer [cols], 4-byte elements
-  uint32_t* counter;           // device, 0 between calls (flagged)
-  uint32_t* flag;              // device pointer of the mapped flag word (flagged)
-  uint32_t seq;                // tag / flag value of this call (never 0), unless seq_dev is set:
-  const uint32_t* seq_dev;     // device word holding the call's seq (written by the call's own H2D copy,
-                               // so one captured graph serves every call of a session)
+  const void* pull;            // device pointer of the mapped staging payload, or nullptr (v already on the device)
+  uint32_t pull_bytes;         // payload bytes (multiple of 16): v, then the seq word
+  uint32_t seq_off;            // byte offset of the seq word in the payload
+  uint32_t* sync;              // device 64-bit arrival counter (pull only), zero-initialised once
+  uint32_t seq;                // tag of this call when pull == nullptr
 };
+
+// True when multiply() of a vector of type vt (result type vt) on this index is one single-split
+// scatter launch that can pull and publish (int32, or fp32 within the fixed-point limits).
+bool publishes(const rsr_index_desc& d, rsr_dtype vt);
 
 // multiply.cu: one fused multiply over blocks [b0, b1).  With `pub`, a single-split scatter
 // launch with int32 / fp32 results also publishes them (then *published = true); otherwise the

@@ -1,17 +1,17 @@
 // Host-buffer sessions: the end-to-end call a reference-side binding makes
 // (`multiply_ternary(numpy v, idx)`, kernels.py:196-206 — host vector in, fresh host result out).
 //
-// A session owns, for one index, pinned staging for v, a device copy of v and of the result,
-// and mapped pinned result memory, allocated once and reused every call.  A call is: copy v
-// into the pinned staging while classifying it (host_stage.cpp: integer-valued vectors run on
-// the exact int32 kernel when sum |v| fits int32, on the exact wide multiply otherwise), H2D(v),
-// the multiply, and the conversion into the caller's buffer.  A single-split scatter multiply
-// (int32 / fp32 activations, rows <= 16384)
-// publishes its results into the mapped memory itself (csrc/common.cuh Publish: seq-tagged
-// 64-bit words up to 8 K columns, 4-byte results + a fenced completion flag beyond), so no D2H
-// copy and no stream synchronize sit between the kernel and the caller
-// (tools/microbench/sync_probe.cu, session_timeline.cu measured the alternatives on the B200
-// box).  Other forms are followed by a D2H copy and a stream synchronize.
+// A session owns, for one index, mapped pinned staging for v, a device copy of v and of the
+// result, and mapped pinned result memory, allocated once and reused every call.  A call copies
+// v into the staging while classifying it (host_stage.cpp: integer-valued vectors run on the
+// exact int32 kernel when sum |v| fits int32, on the exact wide multiply otherwise).  A
+// single-split scatter multiply (int32 / fp32 activations, rows <= 16384) is then ONE kernel
+// launch (a captured one-node graph after the first call): the kernel pulls the staged v from
+// mapped memory itself and streams each folded block's results into mapped memory as seq-tagged
+// 64-bit words (csrc/common.cuh Publish), which the host converts into the caller's buffer while
+// later blocks still run — no copy node, no D2H, no stream synchronize
+// (tools/microbench/launch_latency.cu, session_timeline.cu measured the alternatives on the B200
+// box).  Other forms are H2D, the multiply, a D2H copy and a stream synchronize.
 #include <emmintrin.h>
 #include <immintrin.h>
 
@@ -36,28 +36,23 @@ size_t dsize(rsr_dtype t) { return (t == RSR_F64 || t == RSR_I64) ? 8 : 4; }
 
 struct rsr_host_session {
   rsr_index_desc desc;
-  void* h_v = nullptr;      // pinned staging [rows], 8 bytes per row
-  bool tagged = false;                      // publish mode (see rsr::Publish)
+  void* h_v = nullptr;                      // pinned, mapped staging [rows], 8 bytes per row (+ the seq word)
+  void* h_v_dev = nullptr;                  // its device address (the kernel's pull source)
   unsigned long long* h_tag = nullptr;      // pinned, mapped [cols] tagged results (seq << 32 | value)
   unsigned long long* h_tag_dev = nullptr;
-  void* h_res = nullptr;                    // pinned, mapped [cols] 4-byte results (flagged)
-  void* h_res_dev = nullptr;
-  uint32_t* h_flag = nullptr;               // pinned, mapped (flagged)
-  uint32_t* h_flag_dev = nullptr;
-  uint32_t* d_counter = nullptr;
+  uint32_t* d_sync = nullptr;               // device pull arrival counters (Publish::sync), int32 and fp32 kinds
   void* h_copy = nullptr;   // pinned [cols], 8 bytes per column (D2H path)
   void* d_v = nullptr;      // [rows], 8 bytes per row
   void* d_out = nullptr;    // [cols], 8 bytes per column
   void* d_wide = nullptr;   // wide-multiply workspace (whole int64 range), allocated on first use
   size_t wide_bytes = 0;
   uint32_t seq = 0;
-  // Publishing calls (int32 / fp32 scatter) replay a captured graph: H2D of v plus the call's
-  // seq word (staged right after v) -> the publishing multiply, one cudaGraphLaunch instead of a
-  // memcpy and a kernel launch (~4 us of host time); [kind: int32, fp32][variant]
+  // Publishing calls replay a captured one-node graph (the pulling, publishing multiply):
+  // [kind: int32, fp32][variant]
   cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   int direct_calls[2][2] = {{0, 0}, {0, 0}};
   cudaStream_t cap = nullptr;
-  size_t seq_off = 0;       // byte offset of the seq word in h_v / d_v
+  size_t seq_off = 0;       // byte offset of the seq word in h_v / d_v (after a 4-byte-element v)
 };
 
 using rsr::cuda_check;
@@ -68,9 +63,7 @@ void session_free(rsr_host_session* h) {
   if (!h) return;
   if (h->h_v) cudaFreeHost(h->h_v);
   if (h->h_tag) cudaFreeHost(h->h_tag);
-  if (h->h_res) cudaFreeHost(h->h_res);
-  if (h->h_flag) cudaFreeHost(h->h_flag);
-  if (h->d_counter) cudaFree(h->d_counter);
+  if (h->d_sync) cudaFree(h->d_sync);
   if (h->h_copy) cudaFreeHost(h->h_copy);
   if (h->d_v) cudaFree(h->d_v);
   if (h->d_out) cudaFree(h->d_out);
@@ -108,31 +101,11 @@ inline double now_us() {
   return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-// Published int32 / fp32 results -> out_host (float64, or the 4-byte vector type).
+// Published (tagged) int32 / fp32 results -> out_host (float64, or the 4-byte vector type).
 rsr_status read_published(rsr_host_session* h, uint32_t seq, rsr_dtype vt, void* out_host, rsr_dtype out_dtype,
                           cudaStream_t s) {
   const rsr_index_desc& d = h->desc;
   rsr_status st = RSR_OK;
-  if (!h->tagged) {
-    // flagged: poll the flag; every few thousand polls ask the stream whether it failed
-    volatile uint32_t* flag = h->h_flag;
-    for (uint32_t spins = 1; *flag != seq; ++spins) {
-      _mm_pause();
-      if ((spins & 1023u) == 0) {
-        const cudaError_t e = cudaStreamQuery(s);
-        if (e == cudaSuccess) {
-          if (*flag != seq) return fail(RSR_ERR_CUDA, "host session: the multiply completed without publishing");
-          break;
-        }
-        if (e != cudaErrorNotReady) return cuda_check(e, "host session multiply");
-      }
-    }
-    std::atomic_thread_fence(std::memory_order_acquire);
-    if (out_dtype == vt) std::memcpy(out_host, h->h_res, 4 * (size_t)d.cols);
-    else if (vt == RSR_I32) convert((const int32_t*)h->h_res, (double*)out_host, d.cols);
-    else convert((const float*)h->h_res, (double*)out_host, d.cols);
-    return RSR_OK;
-  }
   // tagged: every word is accepted once its tag is this call's seq (an aligned 16-byte load sees
   // two whole 64-bit stores); two words per step, SSE2: the tag check, the int32 / fp32 -> fp64
   // conversion and the store.  While a pair is not ready, spin (asking the stream every few
@@ -196,25 +169,15 @@ rsr_status rsr_host_session_create(const rsr_index_desc* desc, rsr_host_session*
   h->seq_off = (4 * (size_t)desc->rows + 15) & ~(size_t)15;  // after a 4-byte-element v
   const size_t vb = std::max(8 * (size_t)desc->rows, h->seq_off + 16);
   const size_t ob = 8 * (size_t)desc->cols;
-  rsr_status st = cuda_check(cudaHostAlloc(&h->h_v, vb, cudaHostAllocDefault), "session pinned v");
+  rsr_status st = cuda_check(cudaHostAlloc(&h->h_v, vb, cudaHostAllocMapped), "session pinned v");
+  if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer(&h->h_v_dev, h->h_v, 0), "session staging mapping");
   if (st == RSR_OK) st = cuda_check(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking), "session capture stream");
-  // tagged words up to 8 K columns, the fenced flag beyond (the host reads 8 vs 4 bytes per
-  // result against a ~4 us fence + arrival; session_timeline.cu / e2e probes)
-  h->tagged = desc->cols <= 8192;
-  if (h->tagged) {
-    if (st == RSR_OK)
-      st = cuda_check(cudaHostAlloc((void**)&h->h_tag, 8 * (size_t)desc->cols, cudaHostAllocMapped), "session mapped result");
-    if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer((void**)&h->h_tag_dev, h->h_tag, 0), "session result mapping");
-    if (st == RSR_OK) std::memset(h->h_tag, 0, 8 * (size_t)desc->cols);  // tag 0: no call's result
-  } else {
-    if (st == RSR_OK) st = cuda_check(cudaHostAlloc(&h->h_res, 4 * (size_t)desc->cols, cudaHostAllocMapped), "session mapped result");
-    if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer(&h->h_res_dev, h->h_res, 0), "session result mapping");
-    if (st == RSR_OK) st = cuda_check(cudaHostAlloc((void**)&h->h_flag, 64, cudaHostAllocMapped), "session flag");
-    if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer((void**)&h->h_flag_dev, h->h_flag, 0), "session flag mapping");
-    if (st == RSR_OK) st = cuda_check(cudaMalloc((void**)&h->d_counter, 64), "session counter");
-    if (st == RSR_OK) st = cuda_check(cudaMemset(h->d_counter, 0, 64), "session counter init");
-    if (st == RSR_OK) *h->h_flag = 0;
-  }
+  if (st == RSR_OK)
+    st = cuda_check(cudaHostAlloc((void**)&h->h_tag, 8 * (size_t)desc->cols, cudaHostAllocMapped), "session mapped result");
+  if (st == RSR_OK) st = cuda_check(cudaHostGetDevicePointer((void**)&h->h_tag_dev, h->h_tag, 0), "session result mapping");
+  if (st == RSR_OK) std::memset(h->h_tag, 0, 8 * (size_t)desc->cols);  // tag 0: no call's result
+  if (st == RSR_OK) st = cuda_check(cudaMalloc((void**)&h->d_sync, 64), "session pull counter");
+  if (st == RSR_OK) st = cuda_check(cudaMemset(h->d_sync, 0, 64), "session pull counter init");
   if (st == RSR_OK) st = cuda_check(cudaHostAlloc(&h->h_copy, ob, cudaHostAllocDefault), "session pinned result");
   if (st == RSR_OK) st = cuda_check(cudaMalloc(&h->d_v, vb), "session device v");
   if (st == RSR_OK) st = cuda_check(cudaMalloc(&h->d_out, ob), "session device result");
@@ -252,45 +215,25 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, rs
   const rsr_dtype kt = cls.kind == rsr::kStageI32 ? RSR_I32 : cls.kind == rsr::kStageWide ? RSR_I64
                        : cls.kind == rsr::kStageF32 ? RSR_F32 : RSR_F64;  // computed (and staged) type
   const size_t vb = rsr::dsize(kt) * (size_t)d.rows;
-  const bool graph_kind = kt == RSR_I32 || kt == RSR_F32;  // publishing kinds: the H2D is part of the graph
   rsr_status st = RSR_OK;
-  if (!graph_kind || !h->graph[kt == RSR_I32 ? 0 : 1][variant == RSR_VARIANT_RSRPP ? 1 : 0])
-    st = cuda_check(cudaMemcpyAsync(h->d_v, h->h_v, graph_kind ? h->seq_off + 16 : vb, cudaMemcpyHostToDevice, s),
-                    "H2D v");
-  if (st != RSR_OK) return st;
-  bool published = false;
   rsr_dtype rt = kt;  // device result type
-  if (kt == RSR_I64) {
-    rt = out_dtype == RSR_I64 ? RSR_I64 : RSR_F64;
-    const size_t need = rsr::wide_workspace_bytes(d, 0);
-    if (h->wide_bytes < need) {
-      if (h->d_wide) cudaFree(h->d_wide);
-      h->d_wide = nullptr;
-      h->wide_bytes = 0;
-      if ((st = cuda_check(cudaMalloc(&h->d_wide, need), "session wide workspace")) != RSR_OK) return st;
-      h->wide_bytes = need;
-    }
-    st = rsr::multiply_wide(d, (const int64_t*)h->d_v, cls.max_abs, h->d_out, rt, variant, 0, d.nblocks, h->d_wide,
-                            h->wide_bytes, s);
-  } else {
+  if (rsr::publishes(d, kt)) {
+    // one launch: the kernel pulls the staging (v, then the seq word) and streams tagged results
     const uint32_t seq = ++h->seq == 0 ? ++h->seq : h->seq;  // never 0 (the buffer's initial tag)
     const int gk = kt == RSR_I32 ? 0 : 1, gv = variant == RSR_VARIANT_RSRPP ? 1 : 0;
-    const uint32_t* seq_dev = reinterpret_cast<const uint32_t*>((char*)h->d_v + h->seq_off);
+    *reinterpret_cast<volatile uint32_t*>((char*)h->h_v + h->seq_off) = seq;
+    // (one arrival counter per kind: the int32 and fp32 launches may differ in grid)
+    const rsr::Publish pub{h->h_tag_dev, h->h_v_dev, (uint32_t)(h->seq_off + 16), (uint32_t)h->seq_off, h->d_sync + 8 * gk, 0};
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    // graphs for the 4-byte kinds only (the seq word sits right after a 4-byte-element v)
-    const bool can_graph = graph_kind && cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
-    if (graph_kind) *reinterpret_cast<uint32_t*>((char*)h->h_v + h->seq_off) = seq;
+    const bool can_graph = cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+    bool published = false;
     if (h->graph[gk][gv] == nullptr && can_graph && h->direct_calls[gk][gv] >= 1) {
-      // capture once (after one direct call, which set the kernels' attributes): H2D(v + seq), multiply
-      const rsr::Publish gpub = h->tagged ? rsr::Publish{h->h_tag_dev, nullptr, nullptr, nullptr, 0, seq_dev}
-                                          : rsr::Publish{nullptr, h->h_res_dev, h->d_counter, h->h_flag_dev, 0, seq_dev};
+      // capture once (after one direct call, which set the kernel's attributes)
       cudaGraph_t g = nullptr;
       bool gpublished = false;
-      rsr_status cst = cuda_check(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal), "session capture");
-      if (cst == RSR_OK) {
-        rsr_status a = cuda_check(cudaMemcpyAsync(h->d_v, h->h_v, h->seq_off + 16, cudaMemcpyHostToDevice, h->cap), "H2D v");
-        if (a == RSR_OK)
-          a = rsr::multiply(d, h->d_v, kt, h->d_out, kt, variant, RSR_FORM_AUTO, 0, d.nblocks, h->cap, &gpub, &gpublished);
+      if (cuda_check(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal), "session capture") == RSR_OK) {
+        const rsr_status a = rsr::multiply(d, h->d_v, kt, h->d_out, kt, variant, RSR_FORM_AUTO, 0, d.nblocks, h->cap,
+                                           &pub, &gpublished);
         const cudaError_t e = cudaStreamEndCapture(h->cap, &g);
         if (a == RSR_OK && e == cudaSuccess && gpublished) {
           cudaGraphExec_t ex = nullptr;
@@ -304,24 +247,39 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, rs
       st = cuda_check(cudaGraphLaunch(h->graph[gk][gv], s), "session graph launch");
       published = true;
     } else {
-      if (graph_kind) ++h->direct_calls[gk][gv];
-      const rsr::Publish pub = h->tagged ? rsr::Publish{h->h_tag_dev, nullptr, nullptr, nullptr, seq, nullptr}
-                                         : rsr::Publish{nullptr, h->h_res_dev, h->d_counter, h->h_flag_dev, seq, nullptr};
+      ++h->direct_calls[gk][gv];
       st = rsr::multiply(d, h->d_v, kt, h->d_out, kt, variant, RSR_FORM_AUTO, 0, d.nblocks, s, &pub, &published);
     }
-    if (st == RSR_OK && published) {
-      if (tr) { t1 = now_us(); g_trace.v[1].push_back(t1 - t0); t0 = t1; }
-      // int32 / int64 vectors staged as int32 deliver int32 results
-      const rsr_dtype od = out_dtype == RSR_F64 ? RSR_F64 : kt;
-      if (out_dtype == RSR_I64) {  // int64 vector whose sum fit int32: widen the int32 results
-        st = read_published(h, seq, kt, h->h_copy, RSR_I32, s);
-        if (st == RSR_OK) convert((const int32_t*)h->h_copy, (int64_t*)out_host, d.cols);
-      } else {
-        st = read_published(h, seq, kt, out_host, od, s);
-      }
-      if (tr) g_trace.v[3].push_back(now_us() - t0);
-      return st;
+    if (st == RSR_OK && !published) st = fail(RSR_ERR_CUDA, "host session: the multiply did not publish");
+    if (st != RSR_OK) return st;
+    if (tr) { t1 = now_us(); g_trace.v[1].push_back(t1 - t0); t0 = t1; }
+    // int32 / int64 vectors staged as int32 deliver int32 results
+    const rsr_dtype od = out_dtype == RSR_F64 ? RSR_F64 : kt;
+    if (out_dtype == RSR_I64) {  // int64 vector whose sum fit int32: widen the int32 results
+      st = read_published(h, seq, kt, h->h_copy, RSR_I32, s);
+      if (st == RSR_OK) convert((const int32_t*)h->h_copy, (int64_t*)out_host, d.cols);
+    } else {
+      st = read_published(h, seq, kt, out_host, od, s);
     }
+    if (tr) g_trace.v[3].push_back(now_us() - t0);
+    return st;
+  }
+  st = cuda_check(cudaMemcpyAsync(h->d_v, h->h_v, vb, cudaMemcpyHostToDevice, s), "H2D v");
+  if (st != RSR_OK) return st;
+  if (kt == RSR_I64) {
+    rt = out_dtype == RSR_I64 ? RSR_I64 : RSR_F64;
+    const size_t need = rsr::wide_workspace_bytes(d, 0);
+    if (h->wide_bytes < need) {
+      if (h->d_wide) cudaFree(h->d_wide);
+      h->d_wide = nullptr;
+      h->wide_bytes = 0;
+      if ((st = cuda_check(cudaMalloc(&h->d_wide, need), "session wide workspace")) != RSR_OK) return st;
+      h->wide_bytes = need;
+    }
+    st = rsr::multiply_wide(d, (const int64_t*)h->d_v, cls.max_abs, h->d_out, rt, variant, 0, d.nblocks, h->d_wide,
+                            h->wide_bytes, s);
+  } else {
+    st = rsr::multiply(d, h->d_v, kt, h->d_out, kt, variant, RSR_FORM_AUTO, 0, d.nblocks, s);
   }
   if (st != RSR_OK) return st;
   const size_t ob = rsr::dsize(rt) * (size_t)d.cols;

@@ -193,6 +193,67 @@ __device__ __forceinline__ double pow2d(int e) {  // 2^e for |e| <= 1022
   return __longlong_as_double((long long)(1023 + e) << 52);
 }
 
+// Session pull (see Publish): CTA c copies chunk c of the mapped payload into dst and adds 1 to a
+// 64-bit arrival counter; thread 0 of every CTA waits until the counter reaches the end of its
+// launch's generation (every launch on the counter adds exactly nch, so it never needs resetting).  A CTA
+// that has waited kStealNs (some chunk's CTA not yet resident, e.g. SMs held by a concurrent
+// kernel) copies the whole payload itself: copies are identical, so no CTA ever depends on
+// another being scheduled.  Called by every thread.
+template <typename Trace>
+__device__ __forceinline__ void pull_payload(const Publish& pb, void* dst, Trace&& trace) {
+  constexpr unsigned long long kStealNs = 20000;
+  const uint32_t nch = gridDim.x;
+  const uint32_t csz = ((pb.pull_bytes + nch - 1) / nch + 15u) & ~15u;  // chunk bytes
+  const int t = threadIdx.x;
+  const char* src = reinterpret_cast<const char*>(pb.pull);
+  // .nc loads of the mapped payload (tools/microbench/pull_probe.cu: .cv is 8x slower on sysmem;
+  // no launch ever saw a stale line of the rewritten payload with .ca / .cg / .nc)
+  auto copy = [&](uint32_t lo, uint32_t hi) {
+    for (uint32_t o = lo + 16u * (uint32_t)t; o < hi; o += 16u * blockDim.x) {
+      uint4 q;
+      asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(src + o));
+      *reinterpret_cast<uint4*>((char*)dst + o) = q;
+    }
+  };
+  __shared__ uint32_t sh_steal;
+  {
+    const uint32_t lo = min(pb.pull_bytes, blockIdx.x * csz), hi = min(pb.pull_bytes, lo + csz);
+    copy(lo, hi);
+  }
+  __threadfence();
+  __syncthreads();
+  trace(502);
+  if (t == 0) {
+    // this launch's generation from my own arrival (launches on one counter are stream-ordered and
+    // each adds exactly nch): no sysmem read (same-address sysmem reads from many SMs serialise)
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(pb.sync);
+    const unsigned long long old = atomicAdd(ctr, 1ull);
+    const unsigned long long target = (old / nch + 1) * nch;
+    trace(505);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint32_t steal = 0;
+    for (;;) {
+      unsigned long long c;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(ctr) : "memory");
+      if (c >= target) break;
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > kStealNs) { steal = 1; break; }
+    }
+    __threadfence();  // acquire: the other CTAs' chunks before my v loads
+    sh_steal = steal;
+  }
+  __syncthreads();
+  trace(503);
+  if (sh_steal) {
+    trace(504);
+    copy(0, pb.pull_bytes);
+    __threadfence();
+    __syncthreads();
+  }
+}
+
 // FX (fp32 activations): v is quantized once per launch to 31-bit fixed point with a per-CTA
 // power-of-two scale (2^-31 of max|v|, far below fp32 rounding) and accumulated EXACTLY as two
 // 16-bit limbs in two int32 histograms (integer atomics are native; fp32 shared atomics are a
@@ -278,6 +339,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   // v and out may belong to the previous kernel in the stream: wait for it here (PDL)
   if (!p.independent) grid_dependency_wait();
   if (warp == 0) TRACE(4);
+  if (p.pub.pull) pull_payload(p.pub, const_cast<int32_t*>(p.v), [&](int slot) { if (warp == 0) TRACE(slot); });
   if (!p.atomic_out)  // a single-split launch owns its output columns
     for (int i = t; i < nunits * p.k; i += blockDim.x) {
       const int b = p.b_begin + col_cta + (i / p.k) * ncol;
@@ -323,14 +385,14 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     for (int g = 0; g < NG; ++g) {
       const int64_t row = wr0 + 256 * g + 8 * lane;
       const int32_t* vp = p.v + row;
-      if (row + 8 <= p.rows && p.v_aligned) {
-        const int4 a = __ldg(reinterpret_cast<const int4*>(vp));
-        const int4 c = __ldg(reinterpret_cast<const int4*>(vp) + 1);
+      if (row + 8 <= p.rows && p.v_aligned) {  // (.cg: a session pull wrote v during this launch)
+        const int4 a = __ldcg(reinterpret_cast<const int4*>(vp));
+        const int4 c = __ldcg(reinterpret_cast<const int4*>(vp) + 1);
         vr[8 * g + 0] = a.x; vr[8 * g + 1] = a.y; vr[8 * g + 2] = a.z; vr[8 * g + 3] = a.w;
         vr[8 * g + 4] = c.x; vr[8 * g + 5] = c.y; vr[8 * g + 6] = c.z; vr[8 * g + 7] = c.w;
       } else {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? vp[e] : 0;  // rows past the end: 0
+        for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? __ldcg(vp + e) : 0;  // rows past the end: 0
       }
     }
     if constexpr (PACK) {  // packed = v + v2 * 2^16 (mod 2^32)
@@ -470,6 +532,9 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       for (int i = 0; i < MAXNH; ++i) prev[l][i] = 0;
     int fx_e = 0;
     if constexpr (FX) fx_e = fx_exponent(fxmax, nwarps);
+    // tag of the streamed results: the pulled payload's seq word (or the launch's own)
+    const uint32_t pub_seq = p.pub.pull ? __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(p.v) + p.pub.seq_off))
+                                        : p.pub.seq;
     // slot of lane i: 0-7 local bits (< lb), 8-12 lane bits, 13-14 fold-warp bits
     int sh = -1;
     if (lane < 8) sh = lane < lb ? lane : -1;
@@ -710,8 +775,29 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
           long long tot = 0;
 #pragma unroll
           for (int i = 0; i < FW; ++i) tot += fp[i * 16 + lane];
-          out[(int64_t)b * p.k + (w - 1 - sh)] = (OutT)((double)tot * pow2d(-fx_e));
+          const int64_t o = (int64_t)b * p.k + (w - 1 - sh);
+          const float r = (float)((double)tot * pow2d(-fx_e));
+          out[o] = (OutT)r;
+          if (p.pub.tagged)  // streamed publish: this block's columns are final
+            asm volatile("st.global.u64 [%0], %1;" ::"l"(p.pub.tagged + o),
+                         "l"(((unsigned long long)pub_seq << 32) | __float_as_uint(r)) : "memory");
         }
+      } else if (!PACK && p.pub.tagged) {
+        // streamed publish (single split: this CTA owns the block's columns): the fold warps'
+        // slot values summed in shared memory, one store per column to out and to the host
+        int32_t* ip = reinterpret_cast<int32_t*>(fxpart) + (f & 1) * FW * 16;
+        if (lane < 16) ip[fw * 16 + lane] = d[0];
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
+        if (fw == 0 && sh >= 0 && sh < w) {
+          int32_t tot = 0;
+#pragma unroll
+          for (int i = 0; i < FW; ++i) tot += ip[i * 16 + lane];
+          const int64_t o = (int64_t)b * p.k + (w - 1 - sh);
+          out[o] = (OutT)tot;
+          asm volatile("st.global.u64 [%0], %1;" ::"l"(p.pub.tagged + o),
+                       "l"(((unsigned long long)pub_seq << 32) | (uint32_t)tot) : "memory");
+        }
+        CNT(cnt_fold, sh >= 0 && sh < w && d[0] != 0);
       } else {
         if (sh >= 0 && sh < w && d[0] != 0) atomicAdd(out + (int64_t)b * p.k + (w - 1 - sh), (OutT)d[0]);
         CNT(cnt_fold, sh >= 0 && sh < w && d[0] != 0);
@@ -721,42 +807,6 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       if (fw == 0 && f < 40) TRACE(400 + f);
     }
     if (fw == 0) TRACE(6);
-    if (p.pub.tagged || p.pub.host_out) {
-      // publish (host-buffer sessions; single split, so this CTA owns its columns), once every
-      // fold warp has added its share (see Publish)
-      const int ft = fw * 32 + lane;
-      const uint32_t* dout = reinterpret_cast<const uint32_t*>(out);
-      __threadfence();  // my output reductions / stores are performed at L2 before the barrier
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
-      if (fw == 0) TRACE(500);
-      const uint32_t seq = p.pub.seq_dev ? *p.pub.seq_dev : p.pub.seq;
-      const unsigned long long tag = (unsigned long long)seq << 32;
-      uint32_t* hout = reinterpret_cast<uint32_t*>(p.pub.host_out);
-      for (int i = ft; i < nunits * p.k; i += 32 * FW) {
-        const int b = p.b_begin + col_cta + (i / p.k) * ncol;
-        const int c = i % p.k;
-        if (c < block_width(p.cols, p.k, b)) {
-          const int64_t o = (int64_t)b * p.k + c;
-          const uint32_t val = __ldcg(dout + o);
-          if (p.pub.tagged) asm volatile("st.global.u64 [%0], %1;" ::"l"(p.pub.tagged + o), "l"(tag | val) : "memory");
-          else hout[o] = val;
-        }
-      }
-      if (fw == 0) TRACE(501);
-      if (!p.pub.tagged) {
-        // flagged: one gpu-scope release per CTA (after the barrier: cumulative over the CTA's
-        // stores), the last arrival acquires them all, fences at system scope, raises the flag
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
-        if (ft == 0) {
-          __threadfence();
-          if (atomicAdd(p.pub.counter, 1u) == gridDim.x - 1) {
-            __threadfence_system();
-            *p.pub.counter = 0;  // ready for the next call (stream-ordered)
-            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pub.flag), "r"(seq) : "memory");
-          }
-        }
-      }
-    }
   }
   if (warp == 0) TRACE(7);
 #ifdef RSR_COUNT
@@ -1154,12 +1204,16 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   if (publish && p.n_splits == 1) {
     p.pub = *pub;
     if (published) *published = true;
+  } else if (pub && pub->pull) {
+    return fail(RSR_ERR_INVALID, "session pull needs a publishing (single-split int32 / fp32) launch");
   }
+  if (p.pub.pull && (!p.v_aligned || (p.pub.pull_bytes & 15u) || ((uintptr_t)p.pub.pull & 15u)))
+    return fail(RSR_ERR_INVALID, "session pull: 16-byte aligned payload expected");
   const size_t max_smem = device_max_smem_optin();
   const size_t limbs = fx ? 2 : 1;
   auto need = [&](int nh) {  // layout of scatter_kernel's dynamic smem
     return ((sizeof(int32_t) * ((((size_t)1 << d.k) * nh * limbs + 15) & ~(size_t)15) + 127) & ~(size_t)127) +
-           8 * (2 * nh) + 128 /* fxmax */ + (fx ? sizeof(long long) * 2 * kFoldWarps * 16 : 0) /* fxpart */;
+           8 * (2 * nh) + 128 /* fxmax */ + (fx || publish ? sizeof(long long) * 2 * kFoldWarps * 16 : 0) /* fxpart */;
   };
   // the deferred fold wants 3 histogram buffers (2 is the minimum)
   int nhist = need(3) <= max_smem ? 3 : 2;
@@ -1251,6 +1305,10 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
 }
 
 }  // namespace
+
+bool publishes(const rsr_index_desc& d, rsr_dtype vt) {
+  return (vt == RSR_I32 || vt == RSR_F32) && d.k <= 14 && d.rows <= (int64_t)kScatterThreads * kScatterR;
+}
 
 rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
                     rsr_form form, int b0, int b1, cudaStream_t s, const Publish* pub, bool* published,

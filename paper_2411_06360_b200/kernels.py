@@ -179,9 +179,9 @@ _I32_MAX = 2 ** 31 - 1
 
 
 class _HostPlan:
-    """One host-buffer session (rsr_host_session_*: pinned staging, device scratch, mapped
-    result + completion flag) for one index and thread, created on first use and destroyed
-    with the index or the thread."""
+    """One host-buffer session (rsr_host_session_*: mapped staging the kernel pulls v from,
+    device scratch, mapped seq-tagged result words) for one index and thread, created on first
+    use and destroyed with the index or the thread."""
     __slots__ = ("session", "cols", "call", "stream", "__weakref__")
 
     def __init__(self, idx):
@@ -304,7 +304,8 @@ def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_n
 
 def _multiply_host(v_in, idx, use_fold: bool, compute: str | None) -> np.ndarray:
     """Host-buffer path (reference contract): NumPy in, fresh fp64 NumPy out, via one
-    host-buffer session call (stage + classify, H2D, multiply, result)."""
+    host-buffer session call (stage + classify, one pulling / publishing launch or H2D +
+    multiply + D2H, result)."""
     arr = _host_vector(v_in)
     _check_length(arr, idx.rows)
     if compute is None:

@@ -433,11 +433,10 @@ def test_counted_twins_vs_reference(rsr, cuda):
 @pytest.mark.parametrize("rows,cols,k", [(1, 1, 1), (37, 29, 3), (1000, 777, 8), (16384, 1001, 11),
                                          (20000, 515, 12), (2048, 8193, 10), (512, 12001, 9)])
 def test_host_session_all_types(rsr, cuda, rows, cols, k):
-    # (up to 8192 columns the kernel publishes seq-tagged words, beyond it a fenced flag;
-    # rows > 16384 take the D2H path)
-    """NumPy in -> fresh fp64 NumPy out through the host session (H2D, multiply, publish into
-    mapped memory, flag poll): int32 / int64 bit-exact, fp32 within the north-star bound, fp64
-    within the reference's float tolerance; repeated calls reuse the session."""
+    """NumPy in -> fresh fp64 NumPy out through the host session (rows <= 16384: one launch that
+    pulls v from mapped memory and streams seq-tagged results back; rows > 16384 and fp64 /
+    wide kinds: H2D, multiply, D2H): int32 / int64 bit-exact, fp32 within the north-star bound,
+    fp64 within the reference's float tolerance; repeated calls reuse the session."""
     rng = np.random.default_rng([rows, cols, k])
     A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
     idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
@@ -486,6 +485,45 @@ def test_host_session_threads_and_errors(rsr, cuda):
     assert not errors
     with pytest.raises(ValueError, match="does not match"):
         rsr.multiply_ternary(vs[0][:100], idx)
+
+
+def test_host_session_concurrent_streams(rsr, cuda):
+    """Sessions on four non-blocking streams at once, each launch a full 148-CTA grid that pulls
+    its vector from mapped memory (csrc/multiply.cu pull_payload): kernels that cannot all be
+    resident together must neither deadlock nor mix payloads (a CTA whose peers are not running
+    copies the payload itself); int32 and fp32 launches interleave on every session."""
+    import threading
+    import torch
+    rng = np.random.default_rng(11)
+    rows, cols = 16384, 2048
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), 11)
+    vs = [rng.integers(-100, 101, size=rows).astype(np.int32) for _ in range(4)]
+    refs = [c_oracle.naive_ternary(v.astype(np.float64), A) for v in vs]
+    vf = [rng.standard_normal(rows).astype(np.float32) for _ in range(4)]
+    reff = [c_oracle.naive_ternary(v.astype(np.float64), A) for v in vf]
+    errors = []
+
+    def work(i):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                for it in range(40):
+                    if it % 3 == 2:
+                        if not _fp32_ok(rsr.multiply_ternary(vf[i], idx), reff[i]):
+                            errors.append(("fp32", i, it))
+                            return
+                    elif not np.array_equal(rsr.multiply_ternary(vs[i], idx), refs[i]):
+                        errors.append(("int32", i, it))
+                        return
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
 
 
 @pytest.mark.parametrize("rows,cols,k,batch,vmax", [

@@ -39,13 +39,16 @@ static double host_ns() {
 int main() {
   const int64_t n = 16384, m = 16384;
   const int k = 11;
-  rsr_index_desc d{};
+  const int ncopies = getenv("COPIES") ? atoi(getenv("COPIES")) : 1;  // > 1: cold index (rotating copies)
+  std::vector<rsr_index_desc> ds(ncopies);
   size_t pb, sb, bb;
-  CK(rsr_index_layout(n, m, k, 2, &d, &pb, &sb, &bb));
-  for (int h = 0; h < 2; ++h) {
-    CK(cudaMalloc(&d.half[h].perm, pb));
-    CK(cudaMalloc((void**)&d.half[h].seg, sb));
-    CK(cudaMalloc((void**)&d.half[h].bucket, bb));
+  for (auto& d : ds) {
+    CK(rsr_index_layout(n, m, k, 2, &d, &pb, &sb, &bb));
+    for (int h = 0; h < 2; ++h) {
+      CK(cudaMalloc(&d.half[h].perm, pb));
+      CK(cudaMalloc((void**)&d.half[h].seg, sb));
+      CK(cudaMalloc((void**)&d.half[h].bucket, bb));
+    }
   }
   std::vector<int8_t> A(n * m);
   std::mt19937 rng(1);
@@ -53,7 +56,7 @@ int main() {
   int8_t* dA;
   CK(cudaMalloc(&dA, n * m));
   CK(cudaMemcpy(dA, A.data(), n * m, cudaMemcpyHostToDevice));
-  size_t wsb = rsr_preprocess_workspace_bytes(&d);
+  size_t wsb = rsr_preprocess_workspace_bytes(&ds[0]);
   void* ws;
   CK(cudaMalloc(&ws, wsb));
   int32_t* bad;
@@ -61,10 +64,12 @@ int main() {
   CK(cudaMemset(bad, 0, 4));
   cudaStream_t s;
   CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  CK(rsr_preprocess_ternary(dA, m, &d, bad, ws, wsb, s));
-  CK(cudaStreamSynchronize(s));
-  rsr_host_session* sess;
-  CK(rsr_host_session_create(&d, RSR_I32, &sess));
+  std::vector<rsr_host_session*> sess(ncopies);
+  for (int c = 0; c < ncopies; ++c) {
+    CK(rsr_preprocess_ternary(dA, m, &ds[c], bad, ws, wsb, s));
+    CK(cudaStreamSynchronize(s));
+    CK(rsr_host_session_create(&ds[c], &sess[c]));
+  }
   std::vector<int32_t> v(n);
   for (auto& x : v) x = (int32_t)(rng() % 201) - 100;
   std::vector<double> out(m);
@@ -84,10 +89,12 @@ int main() {
   }
   cudaStreamSynchronize(s);
   std::vector<unsigned long long> tr(148 * 512);
+  long steals = 0;
   std::vector<double> rows[10];
-  for (int it = 0; it < 200; ++it) {
+  for (int it = 0; it < 400; ++it) {
     const double t0 = host_ns();
-    CK(rsr_host_session_multiply(sess, v.data(), n * 4, out.data(), m * 8, RSR_F64, RSR_VARIANT_RSRPP, s));
+    CK(rsr_host_session_multiply(sess[it % ncopies], v.data(), RSR_I32, n * 4, out.data(), RSR_F64, m * 8,
+                                 RSR_VARIANT_RSRPP, s));
     const double t1 = host_ns();
     CK(rsr_debug_trace_copy(tr.data(), tr.size()));
     double cs = 1e300, ce = 0, fe = 0, pe = 0, p0 = 0, p1 = 0, p2 = 0, p3 = 0;
@@ -96,14 +103,15 @@ int main() {
       pe = std::max(pe, (double)tr[c * 512 + 1]);
       ce = std::max(ce, (double)tr[c * 512 + 7]);
       fe = std::max(fe, (double)tr[c * 512 + 6]);
-      p0 = std::max(p0, (double)tr[c * 512 + 500]);
-      p1 = std::max(p1, (double)tr[c * 512 + 501]);
-      p2 = std::max(p2, (double)tr[c * 512 + 502]);
-      p3 = std::max(p3, (double)tr[c * 512 + 503]);
+      p0 = std::max(p0, (double)tr[c * 512 + 4]);  // PDL wait passed (the pull starts)
+      p1 = std::max(p1, (double)tr[c * 512 + 502]);  // chunk copied + fenced
+      p2 = std::max(p2, (double)tr[c * 512 + 503]);  // all chunks seen
+      p3 = std::max(p3, (double)tr[c * 512 + 505]);  // arrived (after the calls word came back)
+      if (tr[c * 512 + 504] > tr[c * 512 + 503]) ++steals;
     }
     const double flag_seen = t1 - t0;  // upper bound (includes the host conversion)
     (void)flag_seen;
-    if (it >= 20) {
+    if (it >= 40) {
       rows[0].push_back((t1 - t0) / 1e3);
       rows[1].push_back((cs + off - t0) / 1e3);
       rows[2].push_back((pe + off - t0) / 1e3);
@@ -116,14 +124,15 @@ int main() {
       rows[9].push_back((p3 + off - t0) / 1e3);
     }
   }
-  const char* names[10] = {"call total", "first CTA start", "last prologue end", "last scatter end", "last fold end",
-                           "kernel span", "publish: folds done (last CTA)", "publish: host stores issued",
-                           "publish: (unused)", "publish: (unused)"};
+  const char* names[10] = {"call total", "first CTA start", "last prologue end (v pulled, in registers)",
+                          "last scatter end", "last fold end", "kernel span", "last CTA at the pull",
+                          "last chunk copied", "last CTA past the wait", "last arrival"};
   for (int i = 0; i < 10; ++i) {
     std::sort(rows[i].begin(), rows[i].end());
     printf("%-24s median %7.2f us  (p10 %7.2f  p90 %7.2f)\n", names[i], rows[i][rows[i].size() / 2],
            rows[i][rows[i].size() / 10], rows[i][rows[i].size() * 9 / 10]);
   }
+  printf("CTA-calls that stole the payload: %ld\n", steals);
   printf("(device stamps are shifted by the calibration latency, an upper bound of ~1-2 us)\n");
   return 0;
 }
