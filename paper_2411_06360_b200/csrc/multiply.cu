@@ -381,18 +381,21 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       q1[g] = (TERNARY && ld) ? ld_nc_v4(kb1 + 256 * g) : make_uint4(0, 0, 0, 0);
     }
     int32_t vr[R];
+    const bool pulled = p.pub.pull != nullptr;
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
       const int64_t row = wr0 + 256 * g + 8 * lane;
       const int32_t* vp = p.v + row;
-      if (row + 8 <= p.rows && p.v_aligned) {  // (.cg: a session pull wrote v during this launch)
-        const int4 a = __ldcg(reinterpret_cast<const int4*>(vp));
-        const int4 c = __ldcg(reinterpret_cast<const int4*>(vp) + 1);
+      if (row + 8 <= p.rows && p.v_aligned) {
+        // .nc shares the lines between the CTAs of an SM (small CTAs); .cg when a session pull
+        // wrote v during this launch (the non-coherent path may not see it)
+        const int4 a = pulled ? __ldcg(reinterpret_cast<const int4*>(vp)) : __ldg(reinterpret_cast<const int4*>(vp));
+        const int4 c = pulled ? __ldcg(reinterpret_cast<const int4*>(vp) + 1) : __ldg(reinterpret_cast<const int4*>(vp) + 1);
         vr[8 * g + 0] = a.x; vr[8 * g + 1] = a.y; vr[8 * g + 2] = a.z; vr[8 * g + 3] = a.w;
         vr[8 * g + 4] = c.x; vr[8 * g + 5] = c.y; vr[8 * g + 6] = c.z; vr[8 * g + 7] = c.w;
       } else {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? __ldcg(vp + e) : 0;  // rows past the end: 0
+        for (int e = 0; e < 8; ++e) vr[8 * g + e] = (row + e < p.rows) ? (pulled ? __ldcg(vp + e) : __ldg(vp + e)) : 0;  // rows past the end: 0
       }
     }
     if constexpr (PACK) {  // packed = v + v2 * 2^16 (mod 2^32)
@@ -1162,8 +1165,9 @@ rsr_status launch_scatter_t(const ScatterParams& p, int grid, size_t smem, int t
 
 template <bool PP, typename OutT, bool FX, bool PACK = false>
 rsr_status launch_scatter_fw(const ScatterParams& p, int grid, size_t smem, int threads, int fw, cudaStream_t s) {
-  return fw == 1 ? launch_scatter_t<PP, OutT, FX, 1, PACK>(p, grid, smem, threads, s)
-                 : launch_scatter_t<PP, OutT, FX, kFoldWarps, PACK>(p, grid, smem, threads, s);
+  return fw == 1   ? launch_scatter_t<PP, OutT, FX, 1, PACK>(p, grid, smem, threads, s)
+         : fw == 2 ? launch_scatter_t<PP, OutT, FX, 2, PACK>(p, grid, smem, threads, s)
+                   : launch_scatter_t<PP, OutT, FX, kFoldWarps, PACK>(p, grid, smem, threads, s);
 }
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, void* out, rsr_dtype out_dtype, bool pp,
@@ -1228,11 +1232,13 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   const size_t smem = need(nhist);
   // small CTAs (few rows) share an SM: limits from threads, smem and registers (<= 96 per
   // thread under the launch bounds)
-  // small CTAs run one fold warp so that 4 of them share an SM — when that puts every block in
-  // flight at once (with several blocks per CTA the single fold warp is the slower choice)
-  // (threads < 128: one fold warp always, so that FW = 4 means 4, 8 or 16 scatter warps and
-  // the fold warps form one aligned warpgroup)
-  const int fw = (threads < 128 || (threads == 128 && d.k <= 13 && (b1 - b0) <= 4 * device_sm_count())) ? 1 : kFoldWarps;
+  // fold warps: threads < 128: one (so that FW = 4 means 4, 8 or 16 scatter warps and the fold
+  // warps form one aligned warpgroup)
+  static const int env_fw = getenv("RSR_B200_FOLD_WARPS") ? atoi(getenv("RSR_B200_FOLD_WARPS")) : 0;  // A/B only
+  // 4 scatter warps (rows <= 4096): 2 fold warps for int32 (4096^2 3.74 vs 4.35 us with 1, 4096 x 14336
+  // 7.90 vs 8.34 us with 4), 4 for the two-limb FX fold (4096^2 fp32 6.09 vs 7.20 us with 1)
+  int fw = threads < 128 ? 1 : threads == 128 ? (fx ? kFoldWarps : 2) : kFoldWarps;
+  if (env_fw == 1 || env_fw == 2 || env_fw == kFoldWarps) fw = (threads < 128 && env_fw > 1) ? fw : env_fw;
   const int cta_threads = threads + 32 * fw;
   const int per_sm = std::max<int>(1, (int)std::min<size_t>(std::min(2048 / cta_threads, 65536 / (cta_threads * 96)),
                                                             (228u << 10) / (smem + 1024)));

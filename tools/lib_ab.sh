@@ -1,0 +1,6 @@
+# A/B of two library builds on the kernel-only bench value: tools/lib_ab.sh <alt.so> [configs...]
+alt=$1; shift
+for rep in 1 2; do for c in "$@"; do for lib in "" "$alt"; do
+  RSR_B200_LIB=$lib timeout 300 python bench.py --config $c --no-cpu --steps 400 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$c', '${lib:-current}', round(d['ms_per_step']*1e3,3), 'us')"
+done; done; done
