@@ -25,10 +25,24 @@ constexpr double kTwo63 = 9223372036854775808.0;
 uint64_t uabs64(int64_t x) { return x < 0 ? 0 - (uint64_t)x : (uint64_t)x; }
 
 StageInfo stage_i32(const int32_t* __restrict__ src, int64_t n, void* dst, bool force_i32) {
-  // pass 1: copy and max |v| (3 vector ops per 8 entries); max |v| * n <= 2^31 - 1 bounds the sum
+  // pass 1 (explicit AVX2, two accumulators): copy and max |v|; max |v| * n <= 2^31 - 1 bounds
+  // the sum (|INT32_MIN| reads as 2^31 unsigned, so it never passes)
   int32_t* __restrict__ d = static_cast<int32_t*>(dst);
+  int64_t i = 0;
+  __m256i m0 = _mm256_setzero_si256(), m1 = m0;
+  for (; i + 16 <= n; i += 16) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 8));
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(d + i), a);
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(d + i + 8), b);
+    m0 = _mm256_max_epu32(m0, _mm256_abs_epi32(a));
+    m1 = _mm256_max_epu32(m1, _mm256_abs_epi32(b));
+  }
+  alignas(32) uint32_t mm[8];
+  _mm256_store_si256(reinterpret_cast<__m256i*>(mm), _mm256_max_epu32(m0, m1));
   uint32_t mx = 0;
-  for (int64_t i = 0; i < n; ++i) {
+  for (int e = 0; e < 8; ++e) mx = mm[e] > mx ? mm[e] : mx;
+  for (; i < n; ++i) {
     const int32_t x = src[i];
     d[i] = x;
     const uint32_t a = x < 0 ? 0u - (uint32_t)x : (uint32_t)x;
@@ -63,37 +77,45 @@ StageInfo stage_i64(const int64_t* __restrict__ src, int64_t n, void* dst) {
 }
 
 StageInfo stage_f64(const double* __restrict__ src, int64_t n, void* dst) {
-  // pass 1 (vectorised): clamp to the int32 range, truncate, and check that the round trip
-  // gives x back (NaN / inf and non-integers fail it); sum of |int32 value| in int64
+  // pass 1 (explicit AVX2, two accumulators; the compiler leaves this loop scalar): truncate to
+  // int32 and check that the round trip gives x back — NaN, inf, non-integers and values outside
+  // the int32 range (truncated to INT32_MIN) fail it, except x = -2^31 itself, whose |v| reads as
+  // 2^31 below; max |int32 value| bounds the sum
   int32_t* __restrict__ d = static_cast<int32_t*>(dst);
   int64_t i = 0;
-  const __m256d lo = _mm256_set1_pd(-2147483647.0), hi = _mm256_set1_pd(2147483647.0);
-  __m256d okv = _mm256_castsi256_pd(_mm256_set1_epi64x(-1));
-  __m256i sumv = _mm256_setzero_si256();
-  for (; i + 4 <= n; i += 4) {  // explicit AVX2: the compiler leaves this loop scalar
-    const __m256d x = _mm256_loadu_pd(src + i);
-    const __m128i ci = _mm256_cvttpd_epi32(_mm256_min_pd(_mm256_max_pd(x, lo), hi));
-    _mm_storeu_si128(reinterpret_cast<__m128i*>(d + i), ci);
-    okv = _mm256_and_pd(okv, _mm256_cmp_pd(_mm256_cvtepi32_pd(ci), x, _CMP_EQ_OQ));  // NaN: false
-    sumv = _mm256_add_epi64(sumv, _mm256_cvtepu32_epi64(_mm_abs_epi32(ci)));
+  __m256d ok0 = _mm256_castsi256_pd(_mm256_set1_epi64x(-1)), ok1 = ok0;
+  __m128i mx0 = _mm_setzero_si128(), mx1 = mx0;
+  for (; i + 8 <= n; i += 8) {
+    const __m256d x0 = _mm256_loadu_pd(src + i), x1 = _mm256_loadu_pd(src + i + 4);
+    const __m128i c0 = _mm256_cvttpd_epi32(x0), c1 = _mm256_cvttpd_epi32(x1);
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(d + i), _mm256_set_m128i(c1, c0));
+    ok0 = _mm256_and_pd(ok0, _mm256_cmp_pd(_mm256_cvtepi32_pd(c0), x0, _CMP_EQ_OQ));  // NaN: false
+    ok1 = _mm256_and_pd(ok1, _mm256_cmp_pd(_mm256_cvtepi32_pd(c1), x1, _CMP_EQ_OQ));
+    mx0 = _mm_max_epu32(mx0, _mm_abs_epi32(c0));
+    mx1 = _mm_max_epu32(mx1, _mm_abs_epi32(c1));
   }
-  int ok = _mm256_movemask_pd(okv) == 0xf;
-  alignas(32) int64_t part[4];
-  _mm256_store_si256(reinterpret_cast<__m256i*>(part), sumv);
-  int64_t sum = part[0] + part[1] + part[2] + part[3];
+  int ok = _mm256_movemask_pd(_mm256_and_pd(ok0, ok1)) == 0xf;
+  alignas(16) uint32_t mm[4];
+  _mm_store_si128(reinterpret_cast<__m128i*>(mm), _mm_max_epu32(mx0, mx1));
+  uint32_t mx = 0;
+  for (int e = 0; e < 4; ++e) mx = mm[e] > mx ? mm[e] : mx;
   for (; i < n; ++i) {
     const double x = src[i];
-    double c = x < -2147483647.0 ? -2147483647.0 : x;
-    c = c > 2147483647.0 ? 2147483647.0 : c;
-    const int32_t ci = (int32_t)c;
+    const int32_t ci = _mm_cvttsd_si32(_mm_set_sd(x));  // INT32_MIN out of range, like cvttpd
     d[i] = ci;
     ok &= (double)ci == x;
-    sum += ci < 0 ? -(int64_t)ci : (int64_t)ci;
+    const uint32_t a = ci < 0 ? 0u - (uint32_t)ci : (uint32_t)ci;
+    mx = a > mx ? a : mx;
   }
-  if (ok && sum <= kI32Max) return {kStageI32, 0};
+  if (ok) {
+    if ((uint64_t)mx * (uint64_t)n <= (uint64_t)kI32Max) return {kStageI32, mx};
+    int64_t sum = 0;  // large activations: the exact bound over the staged int32 values
+    for (int64_t j = 0; j < n; ++j) sum += d[j] < 0 ? -(int64_t)d[j] : (int64_t)d[j];
+    if (sum <= kI32Max) return {kStageI32, mx};
+  }
   // pass 2 (rare): finiteness, integrality in the int64 range, max |v|
   bool integral = true;
-  uint64_t mx = 0;
+  uint64_t wmx = 0;
   for (int64_t i = 0; i < n; ++i) {
     const double x = src[i];
     if (!std::isfinite(x)) return {kStageNonFinite, 0};
@@ -101,13 +123,13 @@ StageInfo stage_f64(const double* __restrict__ src, int64_t n, void* dst) {
       integral = false;
     } else {
       const uint64_t a = uabs64((int64_t)x);
-      mx = a > mx ? a : mx;
+      wmx = a > wmx ? a : wmx;
     }
   }
   if (integral) {
     int64_t* __restrict__ w = static_cast<int64_t*>(dst);
     for (int64_t i = 0; i < n; ++i) w[i] = (int64_t)src[i];
-    return {kStageWide, mx};
+    return {kStageWide, wmx};
   }
   std::memcpy(dst, src, (size_t)n * 8);
   return {kStageF64, 0};

@@ -168,3 +168,47 @@ def test_float32_high_dynamic_range(rsr, cuda, ov):
           f"norm-wise = {np.abs(got - ref).max() / np.abs(ref).max():.3e}")
     assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
     assert elem.max() <= 1e-7  # measured 1.9e-8 on the B200
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows", [37, 1003, 16384])
+def test_staging_edge_values(rsr, cuda, rows):
+    """The C staging classifier (csrc/host_stage.cpp, AVX2 body + scalar tail) on the values at
+    its class boundaries, through the host session: exact against integer arithmetic wherever the
+    reference's fp64 result is exact; non-finite entries raise the reference's error."""
+    rng = np.random.default_rng(rows)
+    A = rng.integers(-1, 2, size=(rows, 29), dtype=np.int8)
+    idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), 5)
+    exact = lambda v: [int(x) for x in (A.astype(object).T @ np.asarray(v, dtype=object))]
+
+    def check(v):
+        for form in (v, v.astype(np.float64)) + ((v.astype(np.int32),) if np.abs(v).max() < 2 ** 31 else ()):
+            got = rsr.multiply_ternary(form, idx)
+            assert [int(x) for x in got] == [float(int(e)) for e in exact(v)], (form.dtype, rows)
+
+    base = rng.integers(-100, 101, size=rows).astype(np.int64)
+    for pos in (0, rows - 1, rows // 2):  # the AVX2 body and the scalar tail
+        for val in (-2 ** 31, 2 ** 31 - 1, 2 ** 31, -(2 ** 31) - 1, 2 ** 40):
+            v = base.copy()
+            v[pos] = val
+            check(v)
+    # max |v| * rows > 2^31 - 1 but sum |v| <= 2^31 - 1: the exact-sum branch stays on int32
+    v = np.zeros(rows, np.int64)
+    v[-1] = 2 ** 31 - 2
+    check(v)
+    v[0] = 1
+    check(v)
+    v[1 % rows] += 1  # sum 2^31 (rows >= 2: wide)
+    check(v)
+    # fractional / negative zero: fp64 gather (reference tolerance) and exact zero
+    vf = base.astype(np.float64)
+    vf[rows - 1] += 0.5
+    got = rsr.multiply_ternary(vf, idx)
+    np.testing.assert_allclose(got, A.T.astype(np.float64) @ vf, rtol=1e-9, atol=1e-9)
+    assert np.array_equal(rsr.multiply_ternary(-np.zeros(rows), idx), np.zeros(29))
+    for bad in (np.nan, np.inf, -np.inf):
+        for pos in (0, rows - 1):
+            vb = base.astype(np.float64)
+            vb[pos] = bad
+            with pytest.raises(ValueError, match="finite"):
+                rsr.multiply_ternary(vb, idx)
