@@ -199,11 +199,34 @@ __device__ __forceinline__ double pow2d(int e) {  // 2^e for |e| <= 1022
 // that has waited kStealNs (some chunk's CTA not yet resident, e.g. SMs held by a concurrent
 // kernel) copies the whole payload itself: copies are identical, so no CTA ever depends on
 // another being scheduled.  Called by every thread.
+// The first 16 bytes of this thread's part of its CTA's chunk, loaded at kernel entry so that the
+// sysmem latency (~2.2 us, tools/microbench/pcie_latency.cu) overlaps the prologue.
+struct PullHead {
+  uint4 q;
+  bool has;
+};
+__device__ __forceinline__ uint32_t pull_chunk_bytes(const Publish& pb) {
+  return ((pb.pull_bytes + gridDim.x - 1) / gridDim.x + 15u) & ~15u;
+}
+__device__ __forceinline__ PullHead pull_begin(const Publish& pb) {
+  PullHead h{make_uint4(0, 0, 0, 0), false};
+  const uint32_t csz = pull_chunk_bytes(pb);
+  const uint32_t lo = min(pb.pull_bytes, blockIdx.x * csz), hi = min(pb.pull_bytes, lo + csz);
+  const uint32_t o = lo + 16u * threadIdx.x;
+  if (o < hi) {
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(h.q.x), "=r"(h.q.y), "=r"(h.q.z), "=r"(h.q.w)
+                 : "l"(reinterpret_cast<const char*>(pb.pull) + o));
+    h.has = true;
+  }
+  return h;
+}
+
 template <typename Trace>
-__device__ __forceinline__ void pull_payload(const Publish& pb, void* dst, Trace&& trace) {
+__device__ __forceinline__ void pull_payload(const Publish& pb, const PullHead& head, void* dst, Trace&& trace) {
   constexpr unsigned long long kStealNs = 20000;
   const uint32_t nch = gridDim.x;
-  const uint32_t csz = ((pb.pull_bytes + nch - 1) / nch + 15u) & ~15u;  // chunk bytes
+  const uint32_t csz = pull_chunk_bytes(pb);
   const int t = threadIdx.x;
   const char* src = reinterpret_cast<const char*>(pb.pull);
   // .nc loads of the mapped payload (tools/microbench/pull_probe.cu: .cv is 8x slower on sysmem;
@@ -218,7 +241,8 @@ __device__ __forceinline__ void pull_payload(const Publish& pb, void* dst, Trace
   __shared__ uint32_t sh_steal;
   {
     const uint32_t lo = min(pb.pull_bytes, blockIdx.x * csz), hi = min(pb.pull_bytes, lo + csz);
-    copy(lo, hi);
+    if (head.has) *reinterpret_cast<uint4*>((char*)dst + lo + 16u * t) = head.q;
+    copy(min(hi, lo + 16u * blockDim.x), hi);  // chunks longer than one load per thread (small grids)
   }
   __threadfence();
   __syncthreads();
@@ -307,6 +331,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   OutT* out2 = reinterpret_cast<OutT*>(p.out2);
   const bool is_fold = warp >= nwarps;
   if (warp == 0) TRACE(0);
+  const PullHead pull_head = p.pub.pull ? pull_begin(p.pub) : PullHead{make_uint4(0, 0, 0, 0), false};
   unsigned long long cnt_red = 0, cnt_fold = 0, cnt_redux = 0;  // work counts (RSR_COUNT builds only)
   (void)cnt_red; (void)cnt_fold; (void)cnt_redux;
 
@@ -339,7 +364,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   // v and out may belong to the previous kernel in the stream: wait for it here (PDL)
   if (!p.independent) grid_dependency_wait();
   if (warp == 0) TRACE(4);
-  if (p.pub.pull) pull_payload(p.pub, const_cast<int32_t*>(p.v), [&](int slot) { if (warp == 0) TRACE(slot); });
+  if (p.pub.pull) pull_payload(p.pub, pull_head, const_cast<int32_t*>(p.v), [&](int slot) { if (warp == 0) TRACE(slot); });
   if (!p.atomic_out)  // a single-split launch owns its output columns
     for (int i = t; i < nunits * p.k; i += blockDim.x) {
       const int b = p.b_begin + col_cta + (i / p.k) * ncol;
