@@ -13,7 +13,10 @@ n = m = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 k = rsr.optimal_k_rsrpp(n)
 g = torch.Generator(device="cuda").manual_seed(0)
 A = (torch.randint(0, 3, (n, m), device="cuda", dtype=torch.int8, generator=g) - 1).to(torch.int8)
-idx = rsr.preprocess_ternary(A, k)
+if os.environ.get("TRACE_BINARY"):  # one half: the binary index of the positive entries
+    idx = rsr.preprocess(rsr.BinaryMatrix.from_dense((A == 1).to(torch.uint8).cpu().numpy()), k)
+else:
+    idx = rsr.preprocess_ternary(A, k)
 if os.environ.get("TRACE_F32"):  # fp32 activations: the fixed-point (FX) instance
     v = torch.randn(n, device="cuda", generator=g)
     out = torch.empty(m, dtype=torch.float32, device="cuda")
