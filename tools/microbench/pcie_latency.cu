@@ -37,6 +37,14 @@ __global__ void probe(const uint4* host, uint4* dst, unsigned long long* ctr, un
       dst[blockIdx.x * 28 + t] = q;
       if (MODE == 3) __threadfence();
     }
+  } else if (MODE == 5 || MODE == 6 || MODE == 7) {  // one 4-byte sysmem read: relaxed.sys / volatile / cv
+    if (blockIdx.x == 0 && t == 0) {
+      unsigned x;
+      if (MODE == 5) asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(host) : "memory");
+      if (MODE == 6) asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(x) : "l"(host) : "memory");
+      if (MODE == 7) asm volatile("ld.global.cv.u32 %0, [%1];" : "=r"(x) : "l"(host) : "memory");
+      dst[0].x = x;
+    }
   } else if (MODE == 4) {
     if (t == 0) {
       unsigned long long o = atomicAdd(ctr, 1ull);
@@ -76,6 +84,9 @@ int main() {
   run(probe<2>, 148, "(2) 148 CTAs x 448-byte chunk from sysmem");
   run(probe<3>, 148, "(3) (2) + store + __threadfence");
   run(probe<4>, 148, "(4) 64-bit atomicAdd round trip (148 CTAs, 1 word)");
+  run(probe<5>, 1, "(5) one 4-byte ld.relaxed.sys of sysmem");
+  run(probe<6>, 1, "(6) one 4-byte ld.volatile of sysmem");
+  run(probe<7>, 1, "(7) one 4-byte ld.cv of sysmem");
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
