@@ -230,6 +230,10 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
   uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + (size_t)NBUF * slot_words * 4);
   uint64_t* hfree = hfull + kMaxNbuf;
   int32_t* fpart = reinterpret_cast<int32_t*>(hfree + kMaxNbuf);  // [2][kLaneFold][2][kPlanKb][32] fold partials
+  // per scatter warp: the codes of one 64-row chunk, [4 streams][64 rows] u16, read back with
+  // warp-uniform (broadcast) 16-byte loads (tools/microbench/lds_broadcast.cu: 8 codes per 2.24
+  // cycles against 2 codes per 1.47 cycles for a shuffle)
+  uint16_t* cstage = reinterpret_cast<uint16_t*>(fpart + 2 * kLaneFold * 2 * kPlanKb * 32);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int b = 0; b < NBUF; ++b) {
@@ -340,9 +344,14 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
         uint4 qv[2][2];
         load_v(0, qv[0]);
         if (ng > 1) load_v(1, qv[1]);
+        uint16_t* stg = cstage + warp * (4 * 64);
+        const uint32_t stg_s = smem_u32(stg);
         for (int ch = 0; ch < nch; ++ch) {
           const uint4 qc = qn;
           if (ch + 1 < nch) qn = load_codes(ch + 1);
+          __syncwarp();  // the previous chunk's broadcast reads are done
+          if (c_on) *reinterpret_cast<uint4*>(stg + c_l * 64 + 8 * (lane & 7)) = qc;
+          __syncwarp();
 #pragma unroll
           for (int gg = 0; gg < 8; ++gg) {
             const int g = 8 * ch + gg;
@@ -351,12 +360,17 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
             const uint32_t x8[8] = {qv[d][0].x, qv[d][0].y, qv[d][0].z, qv[d][0].w,
                                     qv[d][1].x, qv[d][1].y, qv[d][1].z, qv[d][1].w};
             if (g + 2 < ng) load_v(g + 2, qv[d]);
+            uint4 cw[NC];  // this group's 8 codes of every stream (warp-uniform 16-byte loads)
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(cw[c].x), "=r"(cw[c].y), "=r"(cw[c].z), "=r"(cw[c].w)
+                           : "r"(stg_s + (uint32_t)(c * 128 + 16 * gg)));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // rows 2k, 2k + 1 of the group
-              const uint32_t src = k == 0 ? qc.x : k == 1 ? qc.y : k == 2 ? qc.z : qc.w;
               uint32_t w[NC];
 #pragma unroll
-              for (int c = 0; c < NC; ++c) w[c] = __shfl_sync(0xffffffffu, src, c * 8 + gg);
+              for (int c = 0; c < NC; ++c) w[c] = k == 0 ? cw[c].x : k == 1 ? cw[c].y : k == 2 ? cw[c].z : cw[c].w;
 #pragma unroll
               for (int hh = 0; hh < 2; ++hh) {
                 const int32_t x = (int32_t)x8[2 * k + hh];
@@ -512,7 +526,8 @@ __global__ void __launch_bounds__((kLaneWarps + kLaneFold) * 32, 1) lanes_kernel
 }
 
 size_t lanes_smem(int slots, int nbuf) {
-  return (size_t)nbuf * slots * 128 + 2 * kMaxNbuf * 8 + 2 * (size_t)kLaneFold * 2 * kPlanKb * 32 * 4;
+  return (size_t)nbuf * slots * 128 + 2 * kMaxNbuf * 8 + 2 * (size_t)kLaneFold * 2 * kPlanKb * 32 * 4 +
+         (size_t)kLaneWarps * 4 * 64 * 2 /* code staging */;
 }
 
 }  // namespace
