@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) kern(const uint4* __restrict__ 
       for (int q = 0; q < 16; ++q) {
         uint32_t x = (uint32_t)(blockIdx.x * 7919 + warp * 104729 + q * 31337 + u) * 2654435761u;
         if (MODE == 4) ad[q] = hbase[q & 1] + (((x >> 8) % NSLOT) << 7);
+        else if (MODE == 11)  // transposed: lane w's words of all slots form one odd-length row
+          ad[q] = (hbase[q & 1] - lane * 4) + (uint32_t)lane * (NSLOT | 1) * 4 + ((x >> 8) % NSLOT) * 4;
         else if (MODE == 5) ad[q] = (hbase[q & 1] - lane * 4) + ((((x >> 3) ^ (lane * 2246822519u)) >> 7) % (NSLOT * 32)) * 4;
         else ad[q] = hbase[q & 1];
       }
@@ -245,6 +247,7 @@ int main() {
   run(kern<3>, d16, "u16 codes + v loads (no REDs)");
   run(kern<4>, d16, "REDs only, conflict-free rows");
   run(kern<5>, d16, "REDs only, random words");
+  run(kern<11>, d16, "REDs only, transposed rows (odd)");
   run(kern<9>, d16t, "lane codes + SHFL + v + REDs (transposed)");
   run(kern<10>, d16t, "lane codes (no SHFL) + v + REDs");
   return 0;
