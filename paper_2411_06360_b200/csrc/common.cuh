@@ -172,6 +172,7 @@ struct Publish {
   uint32_t seq_off;            // byte offset of the seq word in the payload
   uint32_t* sync;              // device 64-bit arrival counter (pull only), zero-initialised once
   uint32_t seq;                // tag of this call when pull == nullptr
+  uint32_t steal_ns;           // pull: a CTA that waited this long for the chunks copies the payload itself
 };
 
 // True when multiply() of a vector of type vt (result type vt) on this index is one single-split

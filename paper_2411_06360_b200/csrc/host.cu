@@ -223,7 +223,10 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, rs
     const int gk = kt == RSR_I32 ? 0 : 1, gv = variant == RSR_VARIANT_RSRPP ? 1 : 0;
     *reinterpret_cast<volatile uint32_t*>((char*)h->h_v + h->seq_off) = seq;
     // (one arrival counter per kind: the int32 and fp32 launches may differ in grid)
-    const rsr::Publish pub{h->h_tag_dev, h->h_v_dev, (uint32_t)(h->seq_off + 16), (uint32_t)h->seq_off, h->d_sync + 8 * gk, 0};
+    // RSR_B200_PULL_STEAL_NS (tests): the chunk wait after which a CTA copies the payload itself
+    static const uint32_t steal_ns = getenv("RSR_B200_PULL_STEAL_NS") ? (uint32_t)atol(getenv("RSR_B200_PULL_STEAL_NS")) : 20000u;
+    const rsr::Publish pub{h->h_tag_dev, h->h_v_dev, (uint32_t)(h->seq_off + 16), (uint32_t)h->seq_off, h->d_sync + 8 * gk, 0,
+                           steal_ns};
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     const bool can_graph = cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
     bool published = false;

@@ -224,7 +224,7 @@ __device__ __forceinline__ PullHead pull_begin(const Publish& pb) {
 
 template <typename Trace>
 __device__ __forceinline__ void pull_payload(const Publish& pb, const PullHead& head, void* dst, Trace&& trace) {
-  constexpr unsigned long long kStealNs = 20000;
+  const unsigned long long kStealNs = pb.steal_ns;
   const uint32_t nch = gridDim.x;
   const uint32_t csz = pull_chunk_bytes(pb);
   const int t = threadIdx.x;

@@ -691,3 +691,34 @@ def test_fused_bitlinear_matches_separate_layers(rsr, cuda):
             assert torch.equal(a, b)
     with pytest.raises(ValueError):
         rsr.FusedBitLinear([Wg, Wu[:1000]])
+
+
+def test_host_session_pull_steal_path(cuda):
+    """The pull's fallback (csrc/multiply.cu pull_payload): with the chunk wait forced to 0 ns
+    every CTA copies the whole payload itself instead of waiting for its peers' chunks — results
+    must be identical (run in a fresh process: the knob is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, "REPO")
+import paper_2411_06360_b200 as rsr
+from oracle import c_oracle
+rng = np.random.default_rng(5)
+for rows, cols, k in ((16384, 1500, 11), (4096, 4096, 10), (3000, 77, 6)):
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+    for it in range(4):
+        v = rng.integers(-100, 101, size=rows)
+        ref = c_oracle.naive_ternary(v.astype(np.float64), A)
+        assert np.array_equal(rsr.multiply_ternary(v.astype(np.float64), idx), ref), (rows, it)
+        vf = rng.standard_normal(rows).astype(np.float32)
+        reff = c_oracle.naive_ternary(vf.astype(np.float64), A)
+        got = rsr.multiply_ternary(vf, idx)
+        assert np.abs(got - reff).max() <= 1e-5 * max(1.0, np.abs(reff).max()), (rows, it)
+print("steal ok")
+'''.replace("REPO", os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, RSR_B200_PULL_STEAL_NS="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "steal ok" in r.stdout, r.stdout + r.stderr
