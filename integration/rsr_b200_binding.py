@@ -58,8 +58,8 @@ def multiply_ternary_oneshot(v, idx, use_fold: bool) -> np.ndarray:
 
 
 class Session:
-    """The inference-loop binding: one host-buffer session per index (pinned staging, device
-    scratch, mapped result), reused every call.  It classifies v while staging it, so integer-
+    """The inference-loop binding: one host-buffer session per index (mapped staging the
+    kernel pulls v from, device scratch, mapped tagged results), reused every call.  It classifies v while staging it, so integer-
     valued vectors (int32 / int64 / fp64 holding integers) are exact (int32 kernel when
     sum |v| fits, the wide multiply otherwise)."""
 
