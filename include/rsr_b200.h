@@ -230,6 +230,20 @@ rsr_status rsr_multiply_batched_plan(const rsr_index_desc* desc, const rsr_batch
                                      int64_t batch, int32_t* OUT, rsr_variant variant, void* workspace,
                                      size_t workspace_bytes, void* stream);
 
+/* Fused all-gather epilogue (multi-GPU column shards; replaces the
+ * multiply_parallel shard launch + the all-gather of the output slices): int32 multiply of all
+ * blocks of `desc` (single row split: rows <= 16384) that ALSO stores every folded block's column
+ * values into peer_out[r][col_base + column] for r < npeers — device pointers of every rank's
+ * gathered vector in peer-mapped (symmetric) memory — then releases its stores at system scope
+ * and adds 1 to every rank's peer_sig[r].  `done` is this rank's local completion counter
+ * (zero-initialised, reused every call).  A rank's gathered vector holds every rank's slice of
+ * call c once its signal reaches c * npeers: rsr_allgather_wait enqueues that wait on a stream
+ * (traps after 4 s if a peer never arrives).  `out` receives this rank's own slice too. */
+rsr_status rsr_multiply_allgather(const rsr_index_desc* desc, const int32_t* v, int32_t* out, rsr_variant variant,
+                                  int32_t* const* peer_out, unsigned long long* const* peer_sig, int32_t npeers,
+                                  int64_t col_base, unsigned long long* done, void* stream);
+rsr_status rsr_allgather_wait(const unsigned long long* sig, unsigned long long target, void* stream);
+
 /* End-to-end entry with HOST buffers (the call a reference-side binding makes):
  * copies v_host -> d_v, multiplies all blocks, copies d_out -> out_host and
  * synchronizes the stream.  d_v / d_out are caller-owned device scratch of the

@@ -31,7 +31,7 @@ EXPORTS = (
     "rsr_dense_plane_words", "rsr_dense_pack_ternary", "rsr_dense_multiply",
     "rsr_dense_i8_words", "rsr_dense_pack_ternary_i8", "rsr_dense_multiply_i8",
     "rsr_batch_plan_layout", "rsr_batch_plan_build", "rsr_multiply_batched_plan_workspace_bytes",
-    "rsr_multiply_batched_plan",
+    "rsr_multiply_batched_plan", "rsr_multiply_allgather", "rsr_allgather_wait",
 )
 
 
@@ -91,6 +91,11 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, I32_, I32_, P]
     L.rsr_multiply.restype = st
+    L.rsr_multiply_allgather.argtypes = [ctypes.POINTER(IndexDesc), P, P, ctypes.c_int, P, P, ctypes.c_int32,
+                                         ctypes.c_int64, P, P]
+    L.rsr_multiply_allgather.restype = st
+    L.rsr_allgather_wait.argtypes = [P, ctypes.c_uint64, P]
+    L.rsr_allgather_wait.restype = st
     L.rsr_multiply_wide_workspace_bytes.argtypes = [ctypes.POINTER(IndexDesc), ctypes.c_uint64]
     L.rsr_multiply_wide_workspace_bytes.restype = SZ
     L.rsr_multiply_wide.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_uint64, P, ctypes.c_int, ctypes.c_int,

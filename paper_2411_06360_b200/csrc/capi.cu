@@ -137,6 +137,26 @@ static rsr_status check_range(const rsr_index_desc* d, int32_t b0, int32_t b1) {
 
 using namespace rsr;
 
+namespace rsr {
+namespace {
+// Stream-ordered wait of a rank for its gathered vector (see common.cuh Gather): one thread polls
+// the rank's signal word at system scope until every rank's launch of this call has arrived.  A
+// peer that never arrives traps after 4 s instead of hanging the stream.
+__global__ void allgather_wait_kernel(const unsigned long long* sig, unsigned long long target) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0, t1, c;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(c) : "l"(sig) : "memory");
+    if (c >= target) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 4000000000ull) __trap();
+    __nanosleep(100);
+  }
+}
+}  // namespace
+}  // namespace rsr
+
 extern "C" {
 
 int rsr_b200_abi_version(void) { return RSR_B200_ABI_VERSION; }
@@ -214,6 +234,32 @@ rsr_status rsr_multiply_wide(const rsr_index_desc* desc, const int64_t* v, uint6
     return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
   return multiply_wide(*desc, v, max_abs, out, out_dtype, variant, block_begin, block_end, workspace, workspace_bytes,
                        (cudaStream_t)stream);
+}
+
+rsr_status rsr_multiply_allgather(const rsr_index_desc* desc, const int32_t* v, int32_t* out, rsr_variant variant,
+                                  int32_t* const* peer_out, unsigned long long* const* peer_sig, int32_t npeers,
+                                  int64_t col_base, unsigned long long* done, void* stream) {
+  if (!desc || !v || !out || !peer_out || !peer_sig || !done) return fail(RSR_ERR_INVALID, "null argument");
+  if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
+    return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
+  if (npeers < 1 || npeers > kMaxPeers) return fail(RSR_ERR_INVALID, "all-gather: 1 to 8 ranks");
+  if (col_base < 0) return fail(RSR_ERR_INVALID, "negative column base");
+  Gather g{};
+  for (int r = 0; r < npeers; ++r) {
+    if (!peer_out[r] || !peer_sig[r]) return fail(RSR_ERR_INVALID, "null peer pointer");
+    g.out[r] = peer_out[r];
+    g.sig[r] = peer_sig[r];
+  }
+  g.done = done;
+  g.npeers = npeers;
+  g.col_base = col_base;
+  return multiply_allgather(*desc, v, out, variant, g, (cudaStream_t)stream);
+}
+
+rsr_status rsr_allgather_wait(const unsigned long long* sig, unsigned long long target, void* stream) {
+  if (!sig) return fail(RSR_ERR_INVALID, "null signal");
+  allgather_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(sig, target);
+  return cuda_check(cudaGetLastError(), "allgather_wait_kernel launch");
 }
 
 rsr_status rsr_batch_plan_layout(const rsr_index_desc* desc, rsr_batch_plan* plan, size_t* code_bytes,

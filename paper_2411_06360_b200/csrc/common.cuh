@@ -175,6 +175,21 @@ struct Publish {
   uint32_t steal_ns;           // pull: a CTA that waited this long for the chunks copies the payload itself
 };
 
+// Fused all-gather epilogue (multi-GPU, csrc/multiply.cu): as soon as a block is folded, every
+// one of its int32 column values is stored into EVERY rank's gathered output (peer pointers into
+// NVLink-mapped symmetric memory: P2P stores overlap the remaining blocks' reductions); each CTA
+// then releases its stores at system scope and counts itself done, and the launch's last CTA
+// adds 1 to every rank's signal word.  A rank's gathered vector is complete when its signal has
+// counted one arrival per rank for this call (rsr_allgather_wait).  Single-split launches only.
+constexpr int kMaxPeers = 8;
+struct Gather {
+  int32_t* out[kMaxPeers];              // each rank's gathered vector (device pointers, peer-mapped)
+  unsigned long long* sig[kMaxPeers];   // each rank's signal word
+  unsigned long long* done;             // this rank's CTA-completion counter (local, zero-initialised)
+  int npeers;                           // 0: no gather
+  int64_t col_base;                     // this rank's first column in the gathered vector
+};
+
 // True when multiply() of a vector of type vt (result type vt) on this index is one single-split
 // scatter launch that can pull and publish (int32, or fp32 within the fixed-point limits).
 bool publishes(const rsr_index_desc& d, rsr_dtype vt);
@@ -188,6 +203,10 @@ bool publishes(const rsr_index_desc& d, rsr_dtype vt);
 rsr_status multiply(const rsr_index_desc& d, const void* v, rsr_dtype vt, void* out, rsr_dtype ot, rsr_variant var,
                     rsr_form form, int b0, int b1, cudaStream_t s, const Publish* pub = nullptr,
                     bool* published = nullptr, bool independent = false);
+// int32 scatter multiply with the fused all-gather epilogue (see Gather); RSR_ERR_UNSUPPORTED when
+// the launch would need row splits.
+rsr_status multiply_allgather(const rsr_index_desc& d, const int32_t* v, int32_t* out, rsr_variant var, const Gather& g,
+                              cudaStream_t s);
 
 // multiply.cu, batched int32 path: the packed-pair guard and the pair multiply.
 // pack_guard: res[0] = max over blocks [0, b1) and logical bins j >= 1 of the bucket load (rows of key j

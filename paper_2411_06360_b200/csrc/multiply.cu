@@ -138,7 +138,8 @@ struct ScatterParams {
   int sched;          // keys stored in scheduled order (k <= 13): butterfly control bits in the codes
   int codes;          // code format: 0 byte offsets in row order, 1 scheduled byte offsets, 2 scheduled word indices
   uint32_t code_mask; // mask of the group's first two code words (clears the control bits)
-  Publish pub;        // host_out != nullptr: also store the results into mapped host memory + flag
+  Publish pub;        // tagged != nullptr: also stream the results into mapped host memory
+  Gather gat;         // npeers > 0: fused all-gather epilogue (see common.cuh Gather)
   int independent;    // no data dependence on the previous launch: skip the grid dependency wait
 };
 
@@ -810,7 +811,7 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
             asm volatile("st.global.u64 [%0], %1;" ::"l"(p.pub.tagged + o),
                          "l"(((unsigned long long)pub_seq << 32) | __float_as_uint(r)) : "memory");
         }
-      } else if (!PACK && p.pub.tagged) {
+      } else if (!PACK && (p.pub.tagged || p.gat.npeers)) {
         // streamed publish (single split: this CTA owns the block's columns): the fold warps'
         // slot values summed in shared memory, one store per column to out and to the host
         int32_t* ip = reinterpret_cast<int32_t*>(fxpart) + (f & 1) * FW * 16;
@@ -822,8 +823,10 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
           for (int i = 0; i < FW; ++i) tot += ip[i * 16 + lane];
           const int64_t o = (int64_t)b * p.k + (w - 1 - sh);
           out[o] = (OutT)tot;
-          asm volatile("st.global.u64 [%0], %1;" ::"l"(p.pub.tagged + o),
-                       "l"(((unsigned long long)pub_seq << 32) | (uint32_t)tot) : "memory");
+          if (p.pub.tagged)
+            asm volatile("st.global.u64 [%0], %1;" ::"l"(p.pub.tagged + o),
+                         "l"(((unsigned long long)pub_seq << 32) | (uint32_t)tot) : "memory");
+          for (int r = 0; r < p.gat.npeers; ++r) p.gat.out[r][p.gat.col_base + o] = tot;  // P2P stores
         }
         CNT(cnt_fold, sh >= 0 && sh < w && d[0] != 0);
       } else {
@@ -835,6 +838,20 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
       if (fw == 0 && f < 40) TRACE(400 + f);
     }
     if (fw == 0) TRACE(6);
+    if (p.gat.npeers && fw == 0) {
+      // fused all-gather: my peer stores released at system scope, then the launch's last CTA
+      // (cumulativity through the completion counter) signals every rank
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_system();
+        const unsigned long long old = atomicAdd(p.gat.done, 1ull);
+        if (old % gridDim.x == gridDim.x - 1) {
+          __threadfence_system();
+          for (int r = 0; r < p.gat.npeers; ++r)
+            asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(p.gat.sig[r]) : "memory");
+        }
+      }
+    }
   }
   if (warp == 0) TRACE(7);
 #ifdef RSR_COUNT
@@ -1197,7 +1214,7 @@ rsr_status launch_scatter_fw(const ScatterParams& p, int grid, size_t smem, int 
 
 rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, void* out, rsr_dtype out_dtype, bool pp,
                             int b0, int b1, cudaStream_t s, const Publish* pub, bool* published, bool independent,
-                            const void* v2 = nullptr, void* out2 = nullptr) {
+                            const void* v2 = nullptr, void* out2 = nullptr, const Gather* gat = nullptr) {
   if (d.k > 14) return fail(RSR_ERR_UNSUPPORTED, "scatter multiply supports k <= 14");
   const bool pack = v2 != nullptr;
   if (pack && (fx || out_dtype != RSR_I32 || pub))
@@ -1206,7 +1223,7 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   p.v2 = reinterpret_cast<const int32_t*>(v2);
   p.out2 = out2;
   p.independent = independent ? 1 : 0;
-  const bool publish = pub && out_dtype != RSR_F64;  // single split only (decided below)
+  const bool publish = (pub && out_dtype != RSR_F64) || gat;  // single split only (decided below)
   for (int h = 0; h < d.halves; ++h) p.key[h] = d.half[h].bucket;
   p.v = reinterpret_cast<const int32_t*>(v);
   p.v_aligned = ((uintptr_t)v & 15) == 0 && ((uintptr_t)v2 & 15) == 0;
@@ -1230,7 +1247,11 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   p.code_mask = p.sched ? kSchedCodeMask : 0xffffffffu;
   p.n_splits = (int)((d.rows + p.rows_per_cta - 1) / p.rows_per_cta);
   p.atomic_out = p.n_splits > 1;
-  if (publish && p.n_splits == 1) {
+  if (gat) {
+    if (p.n_splits != 1 || fx || out_dtype != RSR_I32)
+      return fail(RSR_ERR_UNSUPPORTED, "all-gather epilogue: single-split int32 launches only");
+    p.gat = *gat;
+  } else if (publish && p.n_splits == 1) {
     p.pub = *pub;
     if (published) *published = true;
   } else if (pub && pub->pull) {
@@ -1336,6 +1357,14 @@ rsr_status multiply_gather_t(const rsr_index_desc& d, const void* v, void* out, 
 }
 
 }  // namespace
+
+rsr_status multiply_allgather(const rsr_index_desc& d, const int32_t* v, int32_t* out, rsr_variant var, const Gather& g,
+                              cudaStream_t s) {
+  if (g.npeers < 1 || g.npeers > kMaxPeers) return fail(RSR_ERR_INVALID, "all-gather: 1 to 8 ranks");
+  if (!publishes(d, RSR_I32)) return fail(RSR_ERR_UNSUPPORTED, "all-gather epilogue: single-split int32 launches only");
+  return multiply_scatter(d, v, false, out, RSR_I32, var == RSR_VARIANT_RSRPP, 0, d.nblocks, s, nullptr, nullptr, false,
+                          nullptr, nullptr, &g);
+}
 
 bool publishes(const rsr_index_desc& d, rsr_dtype vt) {
   return (vt == RSR_I32 || vt == RSR_F32) && d.k <= 14 && d.rows <= (int64_t)kScatterThreads * kScatterR;

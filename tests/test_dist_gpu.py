@@ -81,3 +81,70 @@ def test_sharded_multiply_world2_on_gpu(rsr, cuda, rows, cols, k):
     # the two shards cover the columns exactly, split on a block boundary (kernels.py:222)
     assert results[0][1][0] == 0 and results[0][1][1] == results[1][1][0] and results[1][1][1] == cols
     assert results[0][1][1] % k == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols,k,world", [(4096, 1000, 10, 3), (16384, 2050, 11, 4), (300, 77, 6, 8), (1000, 55, 7, 1)])
+def test_fused_allgather_virtual_ranks(rsr, cuda, rows, cols, k, world):
+    """The fused multiply + all-gather kernel (csrc/multiply.cu Gather epilogue) with `world`
+    virtual ranks on one GPU: each rank owns its shard index, its two gathered buffers and its
+    signal word; every rank's launch stores its folded columns into ALL ranks' buffers and signals
+    them.  All launches of a call are enqueued before any wait (no kernel waits on a kernel that
+    is not already queued ahead of it), then each rank's wait + check: every rank's gathered
+    vector equals the unsharded product bitwise, over several calls (both buffer parities)."""
+    import torch
+    from oracle import c_oracle
+    from paper_2411_06360_b200 import dist as D
+    rng = np.random.default_rng([rows, cols, world])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    idxs = [D.preprocess_ternary_shard(A, k, world, r) for r in range(world)]
+    pad = max(D.slice_lengths(cols, k, world))
+    gathered = [torch.full((2, world * pad), -7, dtype=torch.int32, device="cuda") for _ in range(world)]
+    sigs = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
+    dones = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
+    out_ptrs = [(g[0].data_ptr(), g[1].data_ptr()) for g in gathered]
+    sig_ptrs = [s.data_ptr() for s in sigs]
+    fags = [D.FusedAllGather(idxs[r], cols, world, r, out_ptrs, sig_ptrs, gathered[r], dones[r],
+                             variant="rsrpp" if r % 2 == 0 else "rsr") for r in range(world)]
+    for call in range(5):
+        v = rng.integers(-100, 101, size=rows).astype(np.int32)
+        ref = c_oracle.naive_ternary(v.astype(np.float64), A).astype(np.int64)
+        dv = torch.from_numpy(v).cuda()
+        locals_ = [f.launch(dv) for f in fags]
+        for r, f in enumerate(fags):
+            got = f.wait()
+            assert np.array_equal(got.cpu().numpy().astype(np.int64), ref), (call, r)
+            c0, c1 = D.shard_columns(cols, k, world, r)
+            assert np.array_equal(locals_[r].cpu().numpy().astype(np.int64), ref[c0:c1]), (call, r)
+        torch.cuda.synchronize()
+        assert all(int(s.item()) == (call + 1) * world for s in sigs)
+
+
+@pytest.mark.gpu
+def test_fused_allgather_symmetric_world1(rsr, cuda):
+    """The torch symmetric-memory rendezvous path (the multi-GPU plumbing) at world size 1."""
+    import torch
+    import torch.distributed as dist
+    from oracle import c_oracle
+    from paper_2411_06360_b200 import dist as D
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+    except ImportError:  # pragma: no cover
+        pytest.skip("torch symmetric memory unavailable")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(3)
+        A = rng.integers(-1, 2, size=(2048, 700), dtype=np.int8)
+        idx = D.preprocess_ternary_shard(A, 9, 1, 0)
+        try:
+            fag = D.FusedAllGather.symmetric(idx, 700)
+        except Exception as e:  # pragma: no cover - symmetric memory not supported on this box
+            pytest.skip(f"symmetric memory rendezvous failed: {e!r}"[:200])
+        for _ in range(3):
+            v = rng.integers(-100, 101, size=2048).astype(np.int32)
+            got = fag(torch.from_numpy(v).cuda())
+            assert np.array_equal(got.cpu().numpy().astype(np.int64),
+                                  c_oracle.naive_ternary(v.astype(np.float64), A).astype(np.int64))
+    finally:
+        dist.destroy_process_group()
