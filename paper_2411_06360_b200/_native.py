@@ -91,11 +91,12 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, I32_, I32_, P]
     L.rsr_multiply.restype = st
-    L.rsr_multiply_allgather.argtypes = [ctypes.POINTER(IndexDesc), P, P, ctypes.c_int, P, P, ctypes.c_int32,
-                                         ctypes.c_int64, P, P]
-    L.rsr_multiply_allgather.restype = st
-    L.rsr_allgather_wait.argtypes = [P, ctypes.c_uint64, P]
-    L.rsr_allgather_wait.restype = st
+    if hasattr(L, "rsr_multiply_allgather") or not os.environ.get("RSR_B200_LIB"):  # (A/B builds may predate it)
+        L.rsr_multiply_allgather.argtypes = [ctypes.POINTER(IndexDesc), P, P, ctypes.c_int, P, P, ctypes.c_int32,
+                                             ctypes.c_int64, P, P]
+        L.rsr_multiply_allgather.restype = st
+        L.rsr_allgather_wait.argtypes = [P, ctypes.c_uint64, P]
+        L.rsr_allgather_wait.restype = st
     L.rsr_multiply_wide_workspace_bytes.argtypes = [ctypes.POINTER(IndexDesc), ctypes.c_uint64]
     L.rsr_multiply_wide_workspace_bytes.restype = SZ
     L.rsr_multiply_wide.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_uint64, P, ctypes.c_int, ctypes.c_int,

@@ -1,3 +1,6 @@
+#!/bin/bash
+# Bench-only refresh on one GPU: the GPU test suite, every BASELINE config's bench line
+# (gpurun_out/r02_bench/<config>.json), the default line and the reference arm.
 mkdir -p gpurun_out/r02_bench
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 for c in ternary16384 binary16384 llama4096 llama4096x14336 llama14336x4096 ternary4096f32 ternary16384b64 ternary65536 ternary65536s; do
