@@ -535,7 +535,9 @@ def run_ours(args, cfg, dist=None, lite=False):
                  "allgather_exposed_us": ms_per_step * 1e3 - cmed / args.steps * 1e3,
                  "allgather_bytes": world * pad * 4,
                  "overlap": ("all-gather of step i on a comm stream overlaps the multiply of step i+1 "
-                             "(double-buffered slices)") if comm_mode == "overlap" else
+                             "(double-buffered slices; multiply grid capped at "
+                             f"{os.environ.get('RSR_B200_MAX_CTAS', 'all')} CTAs so the collective has SMs)")
+                            if comm_mode == "overlap" else
                             f"serialised all-gather after each multiply ({comm_error})",
                  "gathered_vector_check": "bitwise equal (int32) to the all-gathered per-rank C-oracle slices"
                  if not fp32 else "within 1e-5 norm-wise of the all-gathered per-rank C-oracle slices"}
@@ -860,6 +862,10 @@ def main():
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # leave 4 SMs to the comm stream's all-gather (an NCCL kernel cannot start while the
+        # persistent multiply grid holds every SM); 144 CTAs cost nothing at 16384^2 on one GPU
+        # (22.39 vs 22.43 us: 1490 blocks take 11 rounds either way)
+        os.environ.setdefault("RSR_B200_MAX_CTAS", "144")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = run_ours(args, cfg, dist)

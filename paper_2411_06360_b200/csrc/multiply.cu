@@ -1289,7 +1289,11 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   const int per_sm = std::max<int>(1, (int)std::min<size_t>(std::min(2048 / cta_threads, 65536 / (cta_threads * 96)),
                                                             (228u << 10) / (smem + 1024)));
   const int nblk = b1 - b0;
-  const int sms = device_sm_count();
+  // RSR_B200_MAX_CTAS (read once): leave SMs free for a concurrent collective — the multi-GPU
+  // bench runs the all-gather of step i on a comm stream beside the multiply of step i + 1, and
+  // an NCCL kernel cannot start while a persistent 148-CTA grid holds every SM
+  static const int env_max_ctas = getenv("RSR_B200_MAX_CTAS") ? atoi(getenv("RSR_B200_MAX_CTAS")) : 0;
+  const int sms = env_max_ctas > 0 ? std::min(device_sm_count(), env_max_ctas) : device_sm_count();
   const int ncol = std::max(1, std::min(nblk, sms * per_sm / std::max(1, p.n_splits)));
   const int grid = ncol * p.n_splits;
   if (p.atomic_out) {
