@@ -90,14 +90,14 @@ int main() {
   cudaStreamSynchronize(s);
   std::vector<unsigned long long> tr(148 * 512);
   long steals = 0;
-  std::vector<double> rows[10];
+  std::vector<double> rows[12];
   for (int it = 0; it < 400; ++it) {
     const double t0 = host_ns();
     CK(rsr_host_session_multiply(sess[it % ncopies], v.data(), RSR_I32, n * 4, out.data(), RSR_F64, m * 8,
                                  RSR_VARIANT_RSRPP, s));
     const double t1 = host_ns();
     CK(rsr_debug_trace_copy(tr.data(), tr.size()));
-    double cs = 1e300, ce = 0, fe = 0, pe = 0, p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+    double cs = 1e300, ce = 0, fe = 0, pe = 0, p0 = 0, p1 = 0, p2 = 0, p3 = 0, p4 = 0, p5 = 0;
     for (int c = 0; c < 148; ++c) {
       cs = std::min(cs, (double)tr[c * 512 + 0]);
       pe = std::max(pe, (double)tr[c * 512 + 1]);
@@ -106,7 +106,9 @@ int main() {
       p0 = std::max(p0, (double)tr[c * 512 + 4]);  // PDL wait passed (the pull starts)
       p1 = std::max(p1, (double)tr[c * 512 + 502]);  // chunk copied + fenced
       p2 = std::max(p2, (double)tr[c * 512 + 503]);  // all chunks seen
-      p3 = std::max(p3, (double)tr[c * 512 + 505]);  // arrived (after the calls word came back)
+      p3 = std::max(p3, (double)tr[c * 512 + 505]);  // arrived
+      p4 = std::max(p4, (double)tr[c * 512 + 506]);  // the seq reader saw the call's seq
+      p5 = std::max(p5, (double)tr[c * 512 + 507]);  // past the seq wait (speculative) / start of the copy
       if (tr[c * 512 + 504] > tr[c * 512 + 503]) ++steals;
     }
     const double flag_seen = t1 - t0;  // upper bound (includes the host conversion)
@@ -122,12 +124,15 @@ int main() {
       rows[7].push_back((p1 + off - t0) / 1e3);
       rows[8].push_back((p2 + off - t0) / 1e3);
       rows[9].push_back((p3 + off - t0) / 1e3);
+      rows[10].push_back((p4 + off - t0) / 1e3);
+      rows[11].push_back((p5 + off - t0) / 1e3);
     }
   }
-  const char* names[10] = {"call total", "first CTA start", "last prologue end (v pulled, in registers)",
+  const char* names[12] = {"call total", "first CTA start", "last prologue end (v pulled, in registers)",
                           "last scatter end", "last fold end", "kernel span", "last CTA at the pull",
-                          "last chunk copied", "last CTA past the wait", "last arrival"};
-  for (int i = 0; i < 10; ++i) {
+                          "last chunk copied", "last CTA past the wait", "last arrival", "seq seen by the reader",
+                          "last CTA starting its copy"};
+  for (int i = 0; i < 12; ++i) {
     std::sort(rows[i].begin(), rows[i].end());
     printf("%-24s median %7.2f us  (p10 %7.2f  p90 %7.2f)\n", names[i], rows[i][rows[i].size() / 2],
            rows[i][rows[i].size() / 10], rows[i][rows[i].size() * 9 / 10]);
