@@ -183,6 +183,14 @@ size_t rsr_multiply_wide_workspace_bytes(const rsr_index_desc* desc, uint64_t ma
 rsr_status rsr_multiply_wide(const rsr_index_desc* desc, const int64_t* v, uint64_t max_abs, void* out,
                              rsr_dtype out_dtype, rsr_variant variant, int32_t block_begin, int32_t block_end,
                              void* workspace, size_t workspace_bytes, void* stream);
+/* Fixed-point fp64 (non-integer float64 activations, kernels.py:196-206 computes in fp64):
+ * v_q = round(v * 2^exp2) as int64 (|v_q| <= max_abs < 2^62), multiplied exactly like
+ * rsr_multiply_wide, each column's exact integer rounded once to fp64 and scaled by 2^-exp2.
+ * The host session chooses exp2 so every nonzero |v| keeps >= 41 significant bits (else the fp64
+ * gather kernel runs); the same workspace as rsr_multiply_wide. */
+rsr_status rsr_multiply_fixed(const rsr_index_desc* desc, const int64_t* v_q, uint64_t max_abs, int32_t exp2,
+                              double* out, rsr_variant variant, int32_t block_begin, int32_t block_end, void* workspace,
+                              size_t workspace_bytes, void* stream);
 
 /* Batch plan: the index re-cut for the batch-native kernel (BASELINE config 3, many vectors
  * against one index; the reference has no batch API and runs `multiply_ternary`,

@@ -31,7 +31,7 @@ EXPORTS = (
     "rsr_dense_plane_words", "rsr_dense_pack_ternary", "rsr_dense_multiply",
     "rsr_dense_i8_words", "rsr_dense_pack_ternary_i8", "rsr_dense_multiply_i8",
     "rsr_batch_plan_layout", "rsr_batch_plan_build", "rsr_multiply_batched_plan_workspace_bytes",
-    "rsr_multiply_batched_plan", "rsr_multiply_allgather", "rsr_allgather_wait",
+    "rsr_multiply_batched_plan", "rsr_multiply_allgather", "rsr_allgather_wait", "rsr_multiply_fixed",
 )
 
 
@@ -91,6 +91,10 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, I32_, I32_, P]
     L.rsr_multiply.restype = st
+    if hasattr(L, "rsr_multiply_fixed") or not os.environ.get("RSR_B200_LIB"):  # (A/B builds may predate it)
+        L.rsr_multiply_fixed.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_uint64, ctypes.c_int32, P,
+                                         ctypes.c_int, I32_, I32_, P, SZ, P]
+        L.rsr_multiply_fixed.restype = st
     if hasattr(L, "rsr_multiply_allgather") or not os.environ.get("RSR_B200_LIB"):  # (A/B builds may predate it)
         L.rsr_multiply_allgather.argtypes = [ctypes.POINTER(IndexDesc), P, P, ctypes.c_int, P, P, ctypes.c_int32,
                                              ctypes.c_int64, P, P]

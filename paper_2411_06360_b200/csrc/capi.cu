@@ -31,7 +31,7 @@ size_t batched_plan_workspace_bytes(const rsr_batch_plan& pl, int64_t batch);
 rsr_status multiply_batched_plan(const rsr_index_desc& d, const rsr_batch_plan& pl, const int32_t* V, int64_t batch,
                                  int32_t* out, rsr_variant var, void* ws, size_t ws_bytes, cudaStream_t s);
 rsr_status multiply_wide(const rsr_index_desc& d, const int64_t* v, uint64_t max_abs, void* out, rsr_dtype ot,
-                         rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s);
+                         rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s, int exp2 = 0);
 size_t dense_plane_words(int64_t rows, int64_t cols);
 size_t dense_i8_words(int64_t rows, int64_t cols);
 rsr_status dense_pack_i8(const int8_t* A, int64_t lda, int64_t rows, int64_t cols, uint32_t* Q, int32_t* bad,
@@ -234,6 +234,18 @@ rsr_status rsr_multiply_wide(const rsr_index_desc* desc, const int64_t* v, uint6
     return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
   return multiply_wide(*desc, v, max_abs, out, out_dtype, variant, block_begin, block_end, workspace, workspace_bytes,
                        (cudaStream_t)stream);
+}
+
+rsr_status rsr_multiply_fixed(const rsr_index_desc* desc, const int64_t* v_q, uint64_t max_abs, int32_t exp2,
+                              double* out, rsr_variant variant, int32_t block_begin, int32_t block_end, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  rsr_status st = check_range(desc, block_begin, block_end);
+  if (st != RSR_OK) return st;
+  if (!v_q || !out) return fail(RSR_ERR_INVALID, "null vector or output");
+  if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
+    return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
+  return multiply_wide(*desc, v_q, max_abs, out, RSR_F64, variant, block_begin, block_end, workspace, workspace_bytes,
+                       (cudaStream_t)stream, exp2);
 }
 
 rsr_status rsr_multiply_allgather(const rsr_index_desc* desc, const int32_t* v, int32_t* out, rsr_variant variant,

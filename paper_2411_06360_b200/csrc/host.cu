@@ -28,7 +28,7 @@
 namespace rsr {
 size_t wide_workspace_bytes(const rsr_index_desc& d, uint64_t max_abs);
 rsr_status multiply_wide(const rsr_index_desc& d, const int64_t* v, uint64_t max_abs, void* out, rsr_dtype ot,
-                         rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s);
+                         rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s, int exp2 = 0);
 namespace {
 size_t dsize(rsr_dtype t) { return (t == RSR_F64 || t == RSR_I64) ? 8 : 4; }
 }  // namespace
@@ -212,7 +212,8 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, rs
   const rsr::StageInfo cls = rsr::stage_vector(v_host, v_dtype, d.rows, h->h_v, out_dtype == RSR_I32);
   if (cls.kind == rsr::kStageNonFinite) return fail(RSR_ERR_INVALID, "vector entries must be finite");
   if (tr) { t1 = now_us(); g_trace.v[0].push_back(t1 - t0); t0 = t1; }
-  const rsr_dtype kt = cls.kind == rsr::kStageI32 ? RSR_I32 : cls.kind == rsr::kStageWide ? RSR_I64
+  const rsr_dtype kt = cls.kind == rsr::kStageI32 ? RSR_I32
+                       : (cls.kind == rsr::kStageWide || cls.kind == rsr::kStageFixed) ? RSR_I64
                        : cls.kind == rsr::kStageF32 ? RSR_F32 : RSR_F64;  // computed (and staged) type
   const size_t vb = rsr::dsize(kt) * (size_t)d.rows;
   rsr_status st = RSR_OK;
@@ -270,7 +271,7 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, rs
   st = cuda_check(cudaMemcpyAsync(h->d_v, h->h_v, vb, cudaMemcpyHostToDevice, s), "H2D v");
   if (st != RSR_OK) return st;
   if (kt == RSR_I64) {
-    rt = out_dtype == RSR_I64 ? RSR_I64 : RSR_F64;
+    rt = (out_dtype == RSR_I64 && cls.kind != rsr::kStageFixed) ? RSR_I64 : RSR_F64;
     const size_t need = rsr::wide_workspace_bytes(d, 0);
     if (h->wide_bytes < need) {
       if (h->d_wide) cudaFree(h->d_wide);
@@ -280,7 +281,7 @@ rsr_status rsr_host_session_multiply(rsr_host_session* h, const void* v_host, rs
       h->wide_bytes = need;
     }
     st = rsr::multiply_wide(d, (const int64_t*)h->d_v, cls.max_abs, h->d_out, rt, variant, 0, d.nblocks, h->d_wide,
-                            h->wide_bytes, s);
+                            h->wide_bytes, s, cls.kind == rsr::kStageFixed ? cls.exp2 : 0);
   } else {
     st = rsr::multiply(d, h->d_v, kt, h->d_out, kt, variant, RSR_FORM_AUTO, 0, d.nblocks, s);
   }

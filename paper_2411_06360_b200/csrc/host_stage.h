@@ -7,11 +7,12 @@
 
 namespace rsr {
 
-enum StageKind { kStageI32 = 0, kStageWide = 1, kStageF32 = 2, kStageF64 = 3, kStageNonFinite = -1 };
+enum StageKind { kStageI32 = 0, kStageWide = 1, kStageF32 = 2, kStageF64 = 3, kStageFixed = 4, kStageNonFinite = -1 };
 
 struct StageInfo {
   int kind;          // StageKind
-  uint64_t max_abs;  // max |v| for the integer classes (0 if unknown)
+  uint64_t max_abs;  // max |v| for the integer classes (0 if unknown); max |v_q| for kStageFixed
+  int exp2 = 0;      // kStageFixed: v_q = round(v * 2^exp2), staged as int64
 };
 
 // Copy v [n] of type t into dst (8 * n bytes of pinned staging) in the representation its class

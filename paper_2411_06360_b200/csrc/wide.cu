@@ -11,6 +11,9 @@
 // the limb results recombine exactly in 128-bit integers:  out = sum_l r_l * 2^(s*l).
 // fp64 results are the exact integer rounded once, so they equal the reference's whenever the
 // reference itself is exact (every partial sum below 2^53).
+// Fixed-point use (exp2 != 0): non-integer fp64 vectors staged as v_q = round(v * 2^exp2) (host
+// staging picks exp2 so every nonzero |v| keeps >= 41 significant bits, csrc/host_stage.cpp);
+// the result is the exact product of v_q rounded once and scaled by 2^-exp2.
 #include <type_traits>
 
 #include "common.cuh"
@@ -40,7 +43,7 @@ __global__ void limb_split_kernel(const int64_t* __restrict__ v, int64_t rows, i
 
 template <typename OutT>
 __global__ void limb_combine_kernel(const int32_t* __restrict__ r, int64_t cols, int L, int s, int64_t c0, int64_t c1,
-                                    OutT* __restrict__ out) {
+                                    double scale, OutT* __restrict__ out) {
   for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += (int64_t)gridDim.x * blockDim.x) {
     __int128 acc = 0;
     for (int l = L - 1; l >= 0; --l) acc = acc * ((__int128)1 << s) + (__int128)r[(int64_t)l * cols + c];
@@ -48,11 +51,12 @@ __global__ void limb_combine_kernel(const int32_t* __restrict__ r, int64_t cols,
       out[c] = (OutT)(int64_t)(uint64_t)acc;
     } else {
       const int64_t lo = (int64_t)acc;
+      // one correctly rounded conversion, then the exact power-of-two scale (fixed-point inputs)
       if ((__int128)lo == acc) {
-        out[c] = (OutT)lo;  // one correctly rounded conversion
-      } else {                // beyond int64 (the reference is inexact there too)
+        out[c] = (OutT)((double)lo * scale);
+      } else {  // beyond int64 (the reference is inexact there too)
         const int64_t hi = (int64_t)(acc >> 64);
-        out[c] = (OutT)((double)hi * 18446744073709551616.0 + (double)(uint64_t)acc);
+        out[c] = (OutT)(((double)hi * 18446744073709551616.0 + (double)(uint64_t)acc) * scale);
       }
     }
   }
@@ -87,8 +91,10 @@ size_t wide_workspace_bytes(const rsr_index_desc& d, uint64_t max_abs) {
 }
 
 rsr_status multiply_wide(const rsr_index_desc& d, const int64_t* v, uint64_t max_abs, void* out, rsr_dtype ot,
-                         rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s) {
+                         rsr_variant var, int b0, int b1, void* ws, size_t ws_bytes, cudaStream_t s, int exp2) {
   if (ot != RSR_I64 && ot != RSR_F64) return fail(RSR_ERR_INVALID, "int64 activations produce int64 or float64");
+  if (exp2 != 0 && ot != RSR_F64) return fail(RSR_ERR_INVALID, "scaled (fixed-point) activations produce float64");
+  if (exp2 < -1000 || exp2 > 1000) return fail(RSR_ERR_INVALID, "fixed-point exponent out of range");
   if (d.rows > ((int64_t)1 << 29)) return fail(RSR_ERR_UNSUPPORTED, "wide multiply supports at most 2^29 rows");
   if (b0 >= b1) return RSR_OK;
   if (!ws || ws_bytes < wide_workspace_bytes(d, max_abs)) return fail(RSR_ERR_INVALID, "wide multiply: workspace too small");
@@ -106,8 +112,9 @@ rsr_status multiply_wide(const rsr_index_desc& d, const int64_t* v, uint64_t max
   if (st != RSR_OK) return st;
   const int64_t c0 = (int64_t)b0 * d.k, c1 = std::min<int64_t>(d.cols, (int64_t)b1 * d.k);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * sms, (c1 - c0 + 255) / 256));
-  if (ot == RSR_I64) limb_combine_kernel<int64_t><<<grid, 256, 0, s>>>(res, d.cols, L, sb, c0, c1, (int64_t*)out);
-  else limb_combine_kernel<double><<<grid, 256, 0, s>>>(res, d.cols, L, sb, c0, c1, (double*)out);
+  const double scale = exp2 == 0 ? 1.0 : ldexp(1.0, -exp2);
+  if (ot == RSR_I64) limb_combine_kernel<int64_t><<<grid, 256, 0, s>>>(res, d.cols, L, sb, c0, c1, 1.0, (int64_t*)out);
+  else limb_combine_kernel<double><<<grid, 256, 0, s>>>(res, d.cols, L, sb, c0, c1, scale, (double*)out);
   return cuda_check(cudaGetLastError(), "limb_combine_kernel launch");
 }
 

@@ -238,25 +238,49 @@ def _check_length(arr: np.ndarray, rows: int) -> None:
         raise ValueError(f"vector length {arr.shape[0]} does not match {rows} rows")
 
 
+class _Class(tuple):
+    """(kind, array, max_abs), plus .exp2 for the fixed-point class."""
+    exp2 = 0
+
+
+def _cls(kind, arr, mx, exp2=0):
+    c = _Class((kind, arr, mx))
+    c.exp2 = exp2
+    return c
+
+
+_FIXED_RANGE = 2.0 ** 21  # max / min nonzero |v| for the fixed-point class (host_stage.cpp)
+_FIXED_MIN_ROWS = 8192   # below it the fp64 gather kernel is faster (host_stage.cpp kFixedMinRows)
+
+
 def classify_host_vector(arr: np.ndarray):
     """(kind, array, max_abs): the computation csrc/host_stage.cpp picks for a host vector,
     restated in NumPy for the paths that do not use a session (multiply_parallel).
     kind "i32": integer-valued with sum |v| <= 2^31 - 1 (int32 kernel, bit-exact);
     "wide": other integer-valued vectors with |v| < 2^63 (exact wide multiply);
-    "f32": float32; "f64": other float64."""
+    "fixed": non-integer float64 with >= 8192 rows and max / min nonzero |v| <= 2^21, as the int64 fixed point
+    round(v * 2^exp2) with |v_q| < 2^62 (`.exp2`; exact integer product, rounded once);
+    "f32": float32; "f64": other float64 (the fp64 gather kernel)."""
     if arr.dtype == np.float32:
         _check_finite(arr)
-        return "f32", arr, 0
+        return _cls("f32", arr, 0)
     if arr.dtype.kind == "f":
         _check_finite(arr)
         if not ((np.abs(arr) < 2.0 ** 63).all() and (arr == np.trunc(arr)).all()):
-            return "f64", arr, 0
+            a = np.abs(arr)
+            amax = float(a.max())
+            nz = a[a > 0]
+            if arr.size >= _FIXED_MIN_ROWS and amax > 0 and amax <= float(nz.min()) * _FIXED_RANGE:
+                e = 61 - (int(np.frexp(amax)[1]) - 1)  # amax * 2^e < 2^62 (ilogb(amax) = frexp exponent - 1)
+                q = np.rint(np.ldexp(arr.astype(np.float64), e)).astype(np.int64)
+                return _cls("fixed", q, int(np.abs(q).max()), e)
+            return _cls("f64", arr, 0)
         arr = arr.astype(np.int64)
     mx = max(abs(int(arr.min())), abs(int(arr.max())))
     total = float(np.abs(arr.astype(np.float64)).sum())  # exact for sums below 2^53
     if total <= _I32_MAX:
-        return "i32", arr.astype(np.int32), mx
-    return "wide", arr.astype(np.int64), mx
+        return _cls("i32", arr.astype(np.int32), mx)
+    return _cls("wide", arr.astype(np.int64), mx)
 
 
 def _run_host(idx, arr: np.ndarray, use_fold: bool) -> np.ndarray:
@@ -277,8 +301,10 @@ def _wide_workspace(idx, max_abs: int, device):
     return torch.empty(max(1, (nbytes + 7) // 8), dtype=torch.int64, device=device), nbytes
 
 
-def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO, max_abs: int = 0):
-    """Device-tensor path: v CUDA tensor [rows] -> CUDA tensor [cols]."""
+def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO, max_abs: int = 0,
+                     exp2: int = 0):
+    """Device-tensor path: v CUDA tensor [rows] -> CUDA tensor [cols].  exp2 != 0: v is the int64
+    fixed point round(v * 2^exp2) of a float64 vector (classify_host_vector), result fp64."""
     import torch
     code = _torch_dtype_code(v)
     if v.dim() != 1 or v.shape[0] < 1:
@@ -290,6 +316,12 @@ def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_n
         out = torch.empty(idx.cols, dtype=v.dtype, device=v.device)
     b0, b1 = block_range if block_range is not None else (0, idx.desc.nblocks)
     variant = _native.VARIANT_RSRPP if use_fold else _native.VARIANT_RSR
+    if code == _native.I64 and exp2:  # fixed-point fp64: exact integer product, rounded once, scaled
+        ws, nbytes = _wide_workspace(idx, max_abs, v.device)
+        _native.check(_native.lib().rsr_multiply_fixed(
+            ctypes.byref(idx.desc), v.data_ptr(), max_abs, exp2, out.data_ptr(), variant, b0, b1,
+            ws.data_ptr(), nbytes, _native.current_stream_ptr()))
+        return out
     if code == _native.I64:  # exact wide multiply (limbs through the int32 kernel)
         ws, nbytes = _wide_workspace(idx, max_abs, v.device)
         _native.check(_native.lib().rsr_multiply_wide(
@@ -381,7 +413,8 @@ def multiply_parallel(v, idx, variant: str = "rsrpp", worker_count: int = 1, *, 
         _check_finite(arr)
         kind, vv, mx = "f64", arr.astype(np.float64), 0
     elif compute in (None, "int32"):
-        kind, vv, mx = classify_host_vector(arr)
+        cls = classify_host_vector(arr)
+        kind, vv, mx = cls
         if compute == "int32" and kind != "i32":
             raise ValueError("compute='int32' needs integer-valued activations with sum |v| <= 2^31 - 1")
     else:
@@ -391,8 +424,9 @@ def multiply_parallel(v, idx, variant: str = "rsrpp", worker_count: int = 1, *, 
         out = torch.empty(idx.cols, dtype=torch.float32, device=dv.device)
     else:  # int32 / wide / fp64 kernels write fp64 directly
         out = torch.empty(idx.cols, dtype=torch.float64, device=dv.device)
+    exp2 = cls.exp2 if compute in (None, "int32") else 0
     for r in ranges:
-        _multiply_device(dv, idx, use_fold, r, out, max_abs=mx)
+        _multiply_device(dv, idx, use_fold, r, out, max_abs=mx, exp2=exp2)
     return out.double().cpu().numpy()
 
 

@@ -25,7 +25,7 @@ from overflow_inputs import CASES, digest, make_inputs  # noqa: E402
 EXACT = ["t_i32_2p20", "t_i64_pm2p20", "t_i64_2p36", "b_i32_pos2p20", "t_f64int_2p20", "t_i64_rows70000"]
 CLASS = {"t_i32_2p20": "wide", "t_i64_pm2p20": "wide", "t_i64_2p36": "wide", "b_i32_pos2p20": "wide",
          "t_f64int_2p20": "wide", "t_i64_2p50": "wide", "t_f64_hdr": "f64", "t_f32_hdr": "f32",
-         "t_f64_rows70000": "f64", "t_i64_rows70000": "wide"}
+         "t_f64_rows70000": "fixed", "t_i64_rows70000": "wide"}
 
 
 @pytest.fixture(scope="module")
@@ -56,8 +56,11 @@ def test_classifier(rsr, ov, name):
     _, v = _inputs(ov, name)
     kind, arr, mx = classify_host_vector(np.asarray(v))
     assert kind == CLASS[name]
-    if kind == "wide":
+    if kind in ("wide", "fixed"):
         assert arr.dtype == np.int64 and mx == int(np.abs(arr).max())
+    if kind == "fixed":  # |v_q| < 2^62 and round(v * 2^exp2)
+        cls = classify_host_vector(np.asarray(v))
+        assert mx < 2 ** 62 and np.array_equal(arr, np.rint(np.ldexp(np.asarray(v, np.float64), cls.exp2)).astype(np.int64))
     small = (np.asarray(v)[:100] // (2 ** 25 if kind == "wide" else 1)).astype(np.int64) % 50
     assert classify_host_vector(small)[0] == "i32"
 
@@ -212,3 +215,30 @@ def test_staging_edge_values(rsr, cuda, rows):
             vb[pos] = bad
             with pytest.raises(ValueError, match="finite"):
                 rsr.multiply_ternary(vb, idx)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols,k", [(1000, 333, 8), (16384, 700, 11), (4096, 4096, 10), (9000, 257, 9)])
+def test_fixed_point_float64(rsr, cuda, rows, cols, k):
+    """Non-integer float64 vectors with a moderate dynamic range take the fixed-point route
+    (host_stage.cpp kStageFixed -> rsr_multiply_fixed): the exact product of round(v * 2^e),
+    rounded once.  Within 2^-40 of the condition sum |v_i A_ij| of the exact (object-arithmetic)
+    product, within the reference's float tolerance of its fp64 result, and bitwise equal
+    between the session (multiply_ternary) and multiply_parallel (same classification)."""
+    from oracle import c_oracle
+    from paper_2411_06360_b200.kernels import classify_host_vector
+    rng = np.random.default_rng([rows, cols, k, 64])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), k)
+    for trial in range(3):
+        v = rng.standard_normal(rows) * 10.0 ** rng.integers(-3, 4)
+        fixed = classify_host_vector(v)[0] == "fixed"
+        assert fixed == (rows >= 8192)  # below 8192 rows the fp64 gather kernel is the faster route
+        got = rsr.multiply_ternary(v, idx)
+        ref = c_oracle.naive_ternary(v, A)
+        cond = np.abs(v) @ np.abs(A.astype(np.float64))
+        np.testing.assert_allclose(got, ref, rtol=1e-9, atol=1e-9)
+        assert (np.abs(got - ref) / cond).max() <= 1e-12
+        assert np.array_equal(rsr.multiply_parallel(v, idx, "rsrpp", 3), got)
+        if fixed:  # exact integers: both variants agree bitwise
+            assert np.array_equal(rsr.multiply_ternary(v, idx, "rsr"), got)
