@@ -402,12 +402,13 @@ def run_ours(args, cfg, dist=None, lite=False):
     comm = torch.cuda.Stream() if world > 1 else None
     peak, peak_kind = _peaks()
 
-    def capture(var, mode, warm=False):
+    def capture(var, mode, warm=False, indep=None):
         """K steps in one CUDA graph.  Step i multiplies index copy i % C into slice buffer
         i % 2; mode "overlap": the slice is all-gathered on the comm stream, which overlaps the
         next step's multiply (the multiply two steps later waits for that gather before reusing
         the buffer); "serial": the all-gather follows each multiply on the same stream; "none"."""
         fold = var != "rsr"
+        indep = (args.launch == "independent") if indep is None else indep
         with_comm = mode == "overlap"
         g = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
@@ -421,7 +422,8 @@ def run_ours(args, cfg, dist=None, lite=False):
                     b = i % 2
                     if done[b] is not None:
                         cap.wait_event(done[b])
-                    K._multiply_device(dv, copies[0] if warm else copies[i % ncopies], fold, None, outs[b][:m])
+                    K._multiply_device(dv, copies[0] if warm else copies[i % ncopies], fold, None, outs[b][:m],
+                                       independent=indep)
                     if mode == "serial":
                         dist.all_gather_into_tensor(gathered[b], outs[b])
                     if with_comm:
@@ -505,6 +507,13 @@ def run_ours(args, cfg, dist=None, lite=False):
         med, ms, cs = timed(g)
         results[var] = (med, ms, cs)
         del g
+        # the timed graph's own results (both slice buffers: the last two steps) against the oracle
+        for b in range(min(2, args.steps)):
+            got_b = outs[b][:m].double().cpu().numpy()
+            ok = np.array_equal(got_b, refs[var]) if not fp32 else \
+                float(np.abs(got_b - refs[var]).max()) <= FP32_TOL * max(1.0, float(np.abs(refs[var]).max()))
+            if not ok:
+                raise SystemExit(f"parity failure: the timed graph's step result ({var}, {args.launch}) differs")
     med, ms, clocks = results[variants[0]]
     ms_per_step = med / args.steps
     kernel_us = ms_per_step * 1e3 if world == 1 else None
@@ -519,6 +528,13 @@ def run_ours(args, cfg, dist=None, lite=False):
         wmed, _, _ = timed(g)
         del g
         warm_us = wmed / args.steps * 1e3
+    # the other launch mode beside the headline (independent stream vs dependent chain)
+    other_us = None
+    if world == 1 and not lite:
+        g = capture(variants[0], "none", indep=args.launch != "independent")
+        omed, _, _ = timed(g)
+        del g
+        other_us = omed / args.steps * 1e3
 
     multi = None
     if world > 1:
@@ -666,6 +682,11 @@ def run_ours(args, cfg, dist=None, lite=False):
                   "l2": f"rotating {ncopies} index copies (>= 4x L2): inputs larger than L2 every step",
                   "form": "scatter (fp32: exact two-limb fixed point)" if fp32 else "scatter (int32, exact)",
                   "variant": variants[0], "preprocess_s": round(preprocess_s, 4),
+                  "launch": ("independent matvecs: each launch starts reducing on the SMs the previous one has "
+                             "freed (RSR_MULTIPLY_INDEPENDENT; its output still waits for the previous launch)")
+                  if args.launch == "independent" else "dependent chain: each launch waits for the previous one",
+                  **({("dependent_chain_us" if args.launch == "independent" else "independent_us"): round(other_us, 3)}
+                     if other_us is not None else {}),
                   **({"l2_warm_us": round(warm_us, 3),
                       "l2_warm_note": "one index copy replayed (L2-resident index when it fits): not the headline"}
                      if warm_us is not None else {}),
@@ -858,6 +879,9 @@ def main():
     ap.add_argument("--config", default="ternary16384", choices=sorted(CONFIGS))
     ap.add_argument("--variant", default="auto", choices=["auto", "rsrpp", "rsr", "both"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--launch", default="independent", choices=["independent", "dependent"],
+                    help="steps as independent matvecs (RSR_MULTIPLY_INDEPENDENT: a launch starts reducing on "
+                         "SMs the previous one has freed) or as a dependent chain (each launch waits for the last)")
     ap.add_argument("--k", type=int, default=0, help="block width override (default: indexer.optimal_k_b200)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-strong", action="store_true", help="N > 1: skip the nested config-5 strong-scaling run")

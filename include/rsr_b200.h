@@ -116,6 +116,17 @@ rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_d
                         rsr_dtype out_dtype, rsr_variant variant, rsr_form form,
                         int32_t block_begin, int32_t block_end, void* stream);
 
+/* rsr_multiply with launch flags.  RSR_MULTIPLY_INDEPENDENT: the caller guarantees that no
+ * kernel still in flight on `stream` writes v (e.g. a stream of matvecs on resident inputs, or
+ * layers sharing one input).  The scatter launch then starts its reductions on the SMs the
+ * previous launch has already freed (programmatic dependent launch) instead of waiting for that
+ * launch to finish; only its writes to out wait, so out keeps stream order and launches still
+ * complete in stream order.  Other forms ignore the flag.  Same results as rsr_multiply. */
+#define RSR_MULTIPLY_INDEPENDENT 1u
+rsr_status rsr_multiply_ex(const rsr_index_desc* desc, const void* v, rsr_dtype v_dtype, void* out,
+                           rsr_dtype out_dtype, rsr_variant variant, rsr_form form,
+                           int32_t block_begin, int32_t block_end, uint32_t flags, void* stream);
+
 /* Replaces `load_index` -> RsrIndex.from_blocks (store.py:49-101, indexer.py:89-129): import
  * a stored index whose per-block arrays are already on the device — d_perm{0,1}: u32
  * [nblocks][rows] stable row orders, d_seg{0,1}: u32 [nblocks][seg_stride] segment starts

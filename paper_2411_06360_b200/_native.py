@@ -19,13 +19,14 @@ VARIANT_RSR, VARIANT_RSRPP = 0, 1
 FORM_AUTO, FORM_SCATTER, FORM_GATHER = 0, 1, 2
 
 ABI_VERSION = 3
+MULTIPLY_INDEPENDENT = 1  # rsr_multiply_ex flag (include/rsr_b200.h)
 
 # Every symbol include/rsr_b200.h declares (tests check the .so exports them all).
 EXPORTS = (
     "rsr_b200_abi_version", "rsr_b200_last_error", "rsr_index_layout",
     "rsr_preprocess_workspace_bytes", "rsr_preprocess_ternary", "rsr_preprocess_binary",
     "rsr_index_import_workspace_bytes", "rsr_index_import",
-    "rsr_multiply", "rsr_multiply_wide_workspace_bytes", "rsr_multiply_wide", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host",
+    "rsr_multiply", "rsr_multiply_ex", "rsr_multiply_wide_workspace_bytes", "rsr_multiply_wide", "rsr_multiply_batched_workspace_bytes", "rsr_multiply_batched", "rsr_multiply_host",
     "rsr_host_session_create", "rsr_host_session_destroy", "rsr_host_session_multiply", "rsr_segmented_sum",
     "rsr_block_product", "rsr_naive_multiply_ternary",
     "rsr_dense_plane_words", "rsr_dense_pack_ternary", "rsr_dense_multiply",
@@ -91,6 +92,10 @@ def lib() -> ctypes.CDLL:
     L.rsr_multiply.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, I32_, I32_, P]
     L.rsr_multiply.restype = st
+    if hasattr(L, "rsr_multiply_ex") or not os.environ.get("RSR_B200_LIB"):  # (A/B builds may predate it)
+        L.rsr_multiply_ex.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_int, P, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_int, I32_, I32_, ctypes.c_uint32, P]
+        L.rsr_multiply_ex.restype = st
     if hasattr(L, "rsr_multiply_fixed") or not os.environ.get("RSR_B200_LIB"):  # (A/B builds may predate it)
         L.rsr_multiply_fixed.argtypes = [ctypes.POINTER(IndexDesc), P, ctypes.c_uint64, ctypes.c_int32, P,
                                          ctypes.c_int, I32_, I32_, P, SZ, P]

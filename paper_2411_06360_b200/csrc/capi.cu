@@ -209,15 +209,23 @@ rsr_status rsr_index_import(const rsr_index_desc* desc, const uint32_t* d_perm0,
                       (cudaStream_t)stream);
 }
 
-rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_dtype, void* out, rsr_dtype out_dtype,
-                        rsr_variant variant, rsr_form form, int32_t block_begin, int32_t block_end, void* stream) {
+rsr_status rsr_multiply_ex(const rsr_index_desc* desc, const void* v, rsr_dtype v_dtype, void* out,
+                           rsr_dtype out_dtype, rsr_variant variant, rsr_form form, int32_t block_begin,
+                           int32_t block_end, uint32_t flags, void* stream) {
   rsr_status st = check_range(desc, block_begin, block_end);
   if (st != RSR_OK) return st;
   if (!v || !out) return fail(RSR_ERR_INVALID, "null vector or output");
   if (variant != RSR_VARIANT_RSR && variant != RSR_VARIANT_RSRPP)
     return fail(RSR_ERR_INVALID, "variant must be rsr or rsrpp");
   if (v_dtype == RSR_I64) return fail(RSR_ERR_INVALID, "int64 activations go through rsr_multiply_wide");
-  return multiply(*desc, v, v_dtype, out, out_dtype, variant, form, block_begin, block_end, (cudaStream_t)stream);
+  if (flags & ~RSR_MULTIPLY_INDEPENDENT) return fail(RSR_ERR_INVALID, "unknown multiply flags");
+  return multiply(*desc, v, v_dtype, out, out_dtype, variant, form, block_begin, block_end, (cudaStream_t)stream,
+                  nullptr, nullptr, (flags & RSR_MULTIPLY_INDEPENDENT) != 0);
+}
+
+rsr_status rsr_multiply(const rsr_index_desc* desc, const void* v, rsr_dtype v_dtype, void* out, rsr_dtype out_dtype,
+                        rsr_variant variant, rsr_form form, int32_t block_begin, int32_t block_end, void* stream) {
+  return rsr_multiply_ex(desc, v, v_dtype, out, out_dtype, variant, form, block_begin, block_end, 0u, stream);
 }
 
 size_t rsr_multiply_wide_workspace_bytes(const rsr_index_desc* desc, uint64_t max_abs) {

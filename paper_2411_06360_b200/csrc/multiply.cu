@@ -140,7 +140,7 @@ struct ScatterParams {
   uint32_t code_mask; // mask of the group's first two code words (clears the control bits)
   Publish pub;        // tagged != nullptr: also stream the results into mapped host memory
   Gather gat;         // npeers > 0: fused all-gather epilogue (see common.cuh Gather)
-  int independent;    // no data dependence on the previous launch: skip the grid dependency wait
+  int independent;    // v not written by any launch still in flight: only the fold warps wait (PDL)
 };
 
 // Logical-order view of one int4 of swizzled bins: element e of the result is logical bin
@@ -362,12 +362,17 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
   }
   for (int i = t; i < hist_words / 4; i += blockDim.x) reinterpret_cast<int4*>(hist)[i] = make_int4(0, 0, 0, 0);
   if (warp == 0) TRACE(3);
-  // v and out may belong to the previous kernel in the stream: wait for it here (PDL)
+  // v and out may belong to the previous kernel in the stream: wait for it here (PDL).
+  // Independent launches (the caller guarantees no kernel still in flight writes v) skip this:
+  // their scatter warps start at once on SMs the previous launch has freed, and only the fold
+  // warps wait, before their first access to out (zeroing included) — so out is ordered after
+  // the previous launch and every launch still completes after its predecessor.
   if (!p.independent) grid_dependency_wait();
   if (warp == 0) TRACE(4);
   if (p.pub.pull) pull_payload(p.pub, pull_head, const_cast<int32_t*>(p.v), [&](int slot) { if (warp == 0) TRACE(slot); });
-  if (!p.atomic_out)  // a single-split launch owns its output columns
-    for (int i = t; i < nunits * p.k; i += blockDim.x) {
+  auto zero_out = [&](int t0, int nt) {
+    if (p.atomic_out) return;  // (row splits: the host zeroes out) a single-split launch owns its columns
+    for (int i = t0; i < nunits * p.k; i += nt) {
       const int b = p.b_begin + col_cta + (i / p.k) * ncol;
       const int c = i % p.k;
       if (c < block_width(p.cols, p.k, b)) {
@@ -375,6 +380,8 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
         if constexpr (PACK) out2[(int64_t)b * p.k + c] = (OutT)0;
       }
     }
+  };
+  if (!p.independent) zero_out(t, blockDim.x);
 
   if (!is_fold) {
     // =========================== scatter warps ===========================
@@ -549,6 +556,11 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     // ============================= fold warps =============================
     __syncthreads();
     const int fw = warp - nwarps;  // fold warp index (FB warp bits)
+    if (p.independent) {  // out belongs to the stream order: wait, zero, then fold
+      grid_dependency_wait();
+      zero_out(t - nwarps * 32, 32 * FW);
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * FW) : "memory");
+    }
     // logical bin j = (fw*32 + lane) * 2^lb + e; lane bits start at lb, fold-warp bits at lb + 5
     int lb = p.k - 5 - FB;  // <= 8
     if (lb < 0) lb = 0;
@@ -1257,6 +1269,7 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   } else if (pub && pub->pull) {
     return fail(RSR_ERR_INVALID, "session pull needs a publishing (single-split int32 / fp32) launch");
   }
+  if (p.pub.pull || p.gat.npeers) p.independent = 0;  // a pull writes v; the all-gather signals peers
   if (p.pub.pull && (!p.v_aligned || (p.pub.pull_bytes & 15u) || ((uintptr_t)p.pub.pull & 15u)))
     return fail(RSR_ERR_INVALID, "session pull: 16-byte aligned payload expected");
   const size_t max_smem = device_max_smem_optin();

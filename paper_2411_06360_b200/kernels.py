@@ -302,9 +302,12 @@ def _wide_workspace(idx, max_abs: int, device):
 
 
 def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_native.FORM_AUTO, max_abs: int = 0,
-                     exp2: int = 0):
+                     exp2: int = 0, independent: bool = False):
     """Device-tensor path: v CUDA tensor [rows] -> CUDA tensor [cols].  exp2 != 0: v is the int64
-    fixed point round(v * 2^exp2) of a float64 vector (classify_host_vector), result fp64."""
+    fixed point round(v * 2^exp2) of a float64 vector (classify_host_vector), result fp64.
+    independent: the caller guarantees no kernel still in flight on the stream writes v, so the
+    launch starts reducing on the SMs the previous launch has freed (rsr_multiply_ex flag
+    RSR_MULTIPLY_INDEPENDENT; out still waits for the previous launch)."""
     import torch
     code = _torch_dtype_code(v)
     if v.dim() != 1 or v.shape[0] < 1:
@@ -327,6 +330,11 @@ def _multiply_device(v, idx, use_fold: bool, block_range=None, out=None, form=_n
         _native.check(_native.lib().rsr_multiply_wide(
             ctypes.byref(idx.desc), v.data_ptr(), max_abs, out.data_ptr(), _torch_dtype_code(out), variant, b0, b1,
             ws.data_ptr(), nbytes, _native.current_stream_ptr()))
+        return out
+    if independent:
+        _native.check(_native.lib().rsr_multiply_ex(
+            ctypes.byref(idx.desc), v.data_ptr(), code, out.data_ptr(), _torch_dtype_code(out),
+            variant, form, b0, b1, _native.MULTIPLY_INDEPENDENT, _native.current_stream_ptr()))
         return out
     _native.check(_native.lib().rsr_multiply(
         ctypes.byref(idx.desc), v.data_ptr(), code, out.data_ptr(), _torch_dtype_code(out),

@@ -722,3 +722,90 @@ print("steal ok")
     env = dict(os.environ, RSR_B200_PULL_STEAL_NS="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "steal ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("rows,cols,k", [(16384, 3000, 11), (4096, 4096, 10), (3000, 77, 6), (20000, 500, 9)])
+def test_independent_launches_keep_stream_order(rsr, cuda, rows, cols, k):
+    """RSR_MULTIPLY_INDEPENDENT (rsr_multiply_ex): a launch starts reducing before the previous
+    one has finished, but its writes to out still wait for it.  Long streams of independent
+    launches — alternating indexes and vectors, several writing the SAME output buffer right
+    after a dependent launch into it, ternary and binary, int32 and fp32 — must give exactly the
+    dependent results, eagerly and replayed from a CUDA graph."""
+    import torch
+    from paper_2411_06360_b200 import kernels as K
+    rng = np.random.default_rng([rows, cols, k, 77])
+    A = rng.integers(-1, 2, size=(rows, cols), dtype=np.int8)
+    idxs = [rsr.preprocess_ternary(rsr.TernaryMatrix(A), k),
+            rsr.preprocess_ternary(rsr.TernaryMatrix(A[:, ::-1].copy()), k)]
+    Ab = rng.integers(0, 2, size=(rows, cols), dtype=np.uint8)
+    bidx = rsr.preprocess(rsr.BinaryMatrix.from_dense(Ab), k)
+    vs = [rng.integers(-100, 101, size=rows).astype(np.int32) for _ in range(3)]
+    dvs = [torch.from_numpy(v).cuda() for v in vs]
+    refs = {(i, j): c_oracle.naive_ternary(vs[j].astype(np.float64), A if i == 0 else A[:, ::-1].copy())
+            for i in range(2) for j in range(3)}
+    shared = torch.empty(cols, dtype=torch.int32, device="cuda")
+    outs = [torch.empty(cols, dtype=torch.int32, device="cuda") for _ in range(4)]
+
+    def stream_of_launches():
+        K._multiply_device(dvs[0], idxs[0], True, None, shared)  # dependent, then independents into it
+        for t in range(24):
+            i, j = t % 2, t % 3
+            K._multiply_device(dvs[j], idxs[i], t % 4 != 3, None, outs[t % 4], independent=True)
+            if t % 5 == 4:
+                K._multiply_device(dvs[j], idxs[i], True, None, shared, independent=True)
+        t_sh = max(t for t in range(24) if t % 5 == 4)  # the last launch into `shared`
+        return [(t % 2, t % 3) for t in range(20, 24)], (t_sh % 2, t_sh % 3)
+
+    last, sh = stream_of_launches()
+    torch.cuda.synchronize()
+    for t, (i, j) in zip(range(20, 24), last):
+        assert np.array_equal(outs[t % 4].cpu().numpy().astype(np.float64), refs[(i, j)]), ("eager", t)
+    assert np.array_equal(shared.cpu().numpy().astype(np.float64), refs[sh])
+    # the same stream captured once and replayed
+    for o in outs + [shared]:
+        o.fill_(-7)
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
+        stream_of_launches()
+    torch.cuda.current_stream().wait_stream(cap)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for t, (i, j) in zip(range(20, 24), last):
+        assert np.array_equal(outs[t % 4].cpu().numpy().astype(np.float64), refs[(i, j)]), ("graph", t)
+    # binary and fp32 forms
+    refb = vs[1].astype(np.float64) @ Ab.astype(np.float64)
+    vf = rng.standard_normal(rows).astype(np.float32)
+    reff = vf.astype(np.float64) @ A.astype(np.float64)
+    dvf = torch.from_numpy(vf).cuda()
+    ob = [K._multiply_device(dvs[1], bidx, t % 2 == 0, independent=True) for t in range(6)]
+    of = [K._multiply_device(dvf, idxs[0], True, independent=True) for t in range(6)]
+    torch.cuda.synchronize()
+    for x in ob:
+        assert np.array_equal(x.cpu().numpy().astype(np.float64), refb)
+    if rows <= 16384:
+        for x in of:
+            assert _fp32_ok(x.cpu().numpy(), reff)
+
+
+def test_multiply_ex_flags(rsr, cuda):
+    """rsr_multiply_ex rejects unknown flags with RSR_ERR_INVALID (and leaves out untouched)."""
+    import ctypes
+    import torch
+    from paper_2411_06360_b200 import _native
+    A = np.random.default_rng(3).integers(-1, 2, size=(64, 20), dtype=np.int8)
+    idx = rsr.preprocess_ternary(rsr.TernaryMatrix(A), 4)
+    dv = torch.ones(64, dtype=torch.int32, device="cuda")
+    out = torch.full((20,), 5, dtype=torch.int32, device="cuda")
+    L = _native.lib()
+    st = L.rsr_multiply_ex(ctypes.byref(idx.desc), dv.data_ptr(), _native.I32, out.data_ptr(), _native.I32,
+                           _native.VARIANT_RSRPP, _native.FORM_AUTO, 0, idx.desc.nblocks, 6,
+                           _native.current_stream_ptr())
+    assert st != 0 and b"flags" in L.rsr_b200_last_error()
+    st = L.rsr_multiply_ex(ctypes.byref(idx.desc), dv.data_ptr(), _native.I32, out.data_ptr(), _native.I32,
+                           _native.VARIANT_RSRPP, _native.FORM_AUTO, 0, idx.desc.nblocks,
+                           _native.MULTIPLY_INDEPENDENT, _native.current_stream_ptr())
+    assert st == 0
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), np.ones(64) @ A.astype(np.float64))
