@@ -47,6 +47,9 @@ constexpr int kMaxK = 16;
 #ifndef RSR_KA
 #define RSR_KA 1
 #endif
+#ifndef RSR_TRIGGER_EARLY
+#define RSR_TRIGGER_EARLY 1
+#endif
 constexpr int KA = RSR_KA;  // scatter kernel: 8-row key groups in flight per lane (divides R / 8)
 
 // =====================================================================================
@@ -530,7 +533,11 @@ __global__ void __launch_bounds__(kScatterThreads + 32 * kFoldWarps, 1) scatter_
     int hb = 0;            // histogram buffer of unit u (u % NH, kept incrementally)
     uint32_t hpar = 1;     // parity of hfree[hb]'s phase to wait for: ((u / NH) - 1) & 1
     for (int u = 0; u < nunits; ++u) {
-      if (u + 1 == nunits) grid_launch_dependents();  // the next grid may start its prologue on freed SMs
+      // PDL trigger: the next grid is launched (its CTAs wait for free SMs and take each one the
+      // moment this grid's CTA on it exits).  Every CTA of this grid is resident by now (grids
+      // never exceed one wave), so triggering early cannot starve it; triggering only at the
+      // last unit left the next launch's latency exposed.
+      if (u == (RSR_TRIGGER_EARLY ? 0 : nunits - 1)) grid_launch_dependents();
       if (lane == 0 && wbytes && u + 1 + S < nunits) prefetch_unit(u + 1 + S);
       const uint32_t Hs = hist_s + (uint32_t)(hb * LIMBS * nbk) * 4u;
       if (warp == 0 && u < 40) TRACE(8 + u * 8 + 0);
