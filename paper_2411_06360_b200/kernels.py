@@ -12,7 +12,8 @@ kernels in librsr_b200.so (see csrc/multiply.cu):
   and on the exact wide multiply otherwise (csrc/wide.cu, limbs + int128
   recombination), so the result equals the reference's fp64 result wherever that
   one is exact (SPEC.md:276); float32 vectors run in fp32 (exact fixed point);
-  other float64 vectors run on the fp64 gather kernel.
+  non-integer float64 vectors run as an exact int64 fixed-point product rounded
+  once (>= 8192 rows, dynamic range <= 2^21) or on the fp64 gather kernel.
 * torch CUDA tensors stay on the device: int32 -> int32 (scatter kernel, int32
   arithmetic modulo 2^32), int64 -> int64 (wide multiply, exact modulo 2^64),
   float32 -> float32, float64 -> float64 (gather kernel).
