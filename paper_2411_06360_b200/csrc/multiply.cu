@@ -1304,16 +1304,20 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   // 4 scatter warps (rows <= 4096): 2 fold warps for int32 (4096^2 3.74 vs 4.35 us with 1, 4096 x 14336
   // 7.90 vs 8.34 us with 4), 4 for the two-limb FX fold (4096^2 fp32 6.09 vs 7.20 us with 1)
   int fw = threads < 128 ? 1 : threads == 128 ? (fx ? kFoldWarps : 2) : kFoldWarps;
-  if (env_fw == 1 || env_fw == 2 || env_fw == kFoldWarps) fw = (threads < 128 && env_fw > 1) ? fw : env_fw;
-  const int cta_threads = threads + 32 * fw;
-  const int per_sm = std::max<int>(1, (int)std::min<size_t>(std::min(2048 / cta_threads, 65536 / (cta_threads * 96)),
-                                                            (228u << 10) / (smem + 1024)));
   const int nblk = b1 - b0;
   // RSR_B200_MAX_CTAS (read once): leave SMs free for a concurrent collective — the multi-GPU
   // bench runs the all-gather of step i on a comm stream beside the multiply of step i + 1, and
   // an NCCL kernel cannot start while a persistent 148-CTA grid holds every SM
   static const int env_max_ctas = getenv("RSR_B200_MAX_CTAS") ? atoi(getenv("RSR_B200_MAX_CTAS")) : 0;
   const int sms = env_max_ctas > 0 ? std::min(device_sm_count(), env_max_ctas) : device_sm_count();
+  // independent launches overlap their neighbours' CTAs: fewer fold warps leave room for more
+  // CTAs per SM (tools/fw_ab.sh, independent stream: 4096^2 fp32 5.32 -> 4.97 us with 2 instead
+  // of 4; 4096 x 14336 int32, several CTA waves, 6.82 -> 6.63 us with 1 instead of 2)
+  if (p.independent && threads == 128) fw = fx ? 2 : (nblk > 3 * sms ? 1 : 2);
+  if (env_fw == 1 || env_fw == 2 || env_fw == kFoldWarps) fw = (threads < 128 && env_fw > 1) ? fw : env_fw;
+  const int cta_threads = threads + 32 * fw;
+  const int per_sm = std::max<int>(1, (int)std::min<size_t>(std::min(2048 / cta_threads, 65536 / (cta_threads * 96)),
+                                                            (228u << 10) / (smem + 1024)));
   const int ncol = std::max(1, std::min(nblk, sms * per_sm / std::max(1, p.n_splits)));
   const int grid = ncol * p.n_splits;
   if (p.atomic_out) {
