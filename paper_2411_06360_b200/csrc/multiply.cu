@@ -1291,7 +1291,10 @@ rsr_status multiply_scatter(const rsr_index_desc& d, const void* v, bool fx, voi
   // diagnostics overrides, read once (an environment scan per launch costs ~1 us of host time)
   static const int env_stages = getenv("RSR_B200_STAGES") ? std::max(0, atoi(getenv("RSR_B200_STAGES"))) : -1;
   static const int env_nhist = getenv("RSR_B200_NHIST") ? std::min(4, std::max(2, atoi(getenv("RSR_B200_NHIST")))) : -1;
-  const int stages = env_stages >= 0 ? env_stages : 3;  // L2 prefetch distance in blocks
+  // L2 bulk prefetch distance in units beyond the next one: 0 (the next unit only) measured best
+  // under independent launches (tools/ab.sh RSR_B200_STAGES: 16384^2 22.18 -> 21.68 us with 0
+  // instead of 3, 14336 x 4096 7.35 -> 7.01, 4096 x 14336 6.62 -> 6.46, binary 14.66 -> 14.49)
+  const int stages = env_stages >= 0 ? env_stages : 0;
   if (env_nhist > 0) nhist = env_nhist;
   p.stages = stages;
   p.nhist = nhist;
