@@ -6,7 +6,7 @@
 //  * SCATTER (int32, and fp32 as exact fixed point) — the reference's own fused driver
 //    `_run_blocks` (kernels.py:127-177): u_b[key_b[r]] += v[r] over rows r.  One persistent
 //    CTA per SM keeps its slice of v in REGISTERS for the whole launch, streams the per-block
-//    key codes straight into registers (L2 bulk prefetch a few blocks ahead), and accumulates
+//    key codes straight into registers (L2 bulk prefetch of the next block), and accumulates
 //    a 2^k-bin histogram with shared-memory int32 reductions in a bank-conflict-minimising
 //    key order chosen at preprocess time (butterfly schedule).  Ternary matrices add +v at
 //    the positive key's bin and -v at the negative key's bin of ONE histogram: the fold is
@@ -159,7 +159,7 @@ __device__ __forceinline__ int4 unswizzle4(int4 q, uint32_t c) {
 //    slice: their v values live in registers for the whole launch.  Each scatter warp streams
 //    its rows' key codes of every column block straight into registers (16-byte
 //    ld.global.nc.L1::no_allocate per 8 rows, software-pipelined one half-block ahead) while
-//    lane 0 keeps S blocks ahead with cp.async.bulk.prefetch.L2, so the register loads hit L2.
+//    lane 0 prefetches the next block (S = 0 further ones) with cp.async.bulk.prefetch.L2.
 //    Keys never touch shared memory: the smem data path (128 B/clk) is the kernel's bound and
 //    belongs to the reductions (tools/microbench/red_stream.cu: TMA->smem->LDS streaming
 //    costs 1.5x the LDG path against concurrent REDs).
